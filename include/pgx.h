@@ -1,0 +1,160 @@
+/*
+ * pgx.h — C ABI of the B200-native polygrain fit hot path (libpgx.so).
+ *
+ * This is the drop-in boundary for the reference's in-process NumPy hot path
+ * (reference = /root/reference/pkg/src/polygrain):
+ *
+ *   pgx_problem_create  replaces  basis.assemble_design_matrix   (basis.py:183-193)
+ *                       + the per-fit ``labels0 = labels - 1``    (optimizer.py:205-207)
+ *                       — no K x P design matrix is ever formed: the grid
+ *                       coordinates (geometry.py:59-71) and the Legendre /
+ *                       monomial features (basis.py:105-142) are regenerated
+ *                       on the device inside the kernels.
+ *   pgx_eval            replaces  objective.evaluate_objective    (objective.py:129-165)
+ *                       (Phi, grad, err, e0 of one fused evaluation; also the
+ *                       bodies of objective() :168-178 and gradient() :181-198)
+ *   pgx_assign          replaces  objective.hard_assign           (objective.py:70-77)
+ *                       + geometry.argmin_labels                   (geometry.py:201-210)
+ *                       without the N x P cost matrix.
+ *   pgx_last_error      carries the message of the exception the reference
+ *                       would raise (errors.py:4-13).
+ *
+ * Conventions
+ *  - theta is K x N row-major (column i = grain i), exactly ParamMatrix.values
+ *    (basis.py:287-327); fp64 by default, fp32 with PGX_THETA_F32.
+ *  - labels are 0-based int64, exactly the reference's ``labels0``.
+ *  - Without PGX_DEVICE_PTRS every pointer argument is HOST memory: the call
+ *    copies theta to the device, runs, copies results back and synchronises.
+ *    With PGX_DEVICE_PTRS they are device pointers and the call is enqueued on
+ *    the problem's stream without synchronising (CUDA-Graph capturable: no
+ *    allocation happens after pgx_problem_create).
+ *  - Results are bit-identical run to run (fixed reduction partitions, fp64
+ *    final reduction, no floating-point atomics) — the GPU analogue of the
+ *    reference's threads == 1 sequential fold (objective.py:155-158).
+ *  - Status codes map onto the reference's exceptions:
+ *      PGX_ERR_INVALID_ARGUMENT -> ValueError      (objective.py:171-175)
+ *      PGX_ERR_RESOURCE         -> ResourceError   (basis.py:185-192)
+ *      PGX_ERR_NUMERICAL        -> NumericalError  (optimizer.py:222-226)
+ *      PGX_ERR_CUDA             -> RuntimeError
+ *  - A handle is used by one host thread at a time.
+ */
+#ifndef PGX_H
+#define PGX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PGX_ABI_VERSION 1
+
+typedef enum {
+    PGX_OK = 0,
+    PGX_ERR_INVALID_ARGUMENT = 1,
+    PGX_ERR_RESOURCE = 2,
+    PGX_ERR_NUMERICAL = 3,
+    PGX_ERR_CUDA = 4
+} pgx_status;
+
+/* basis kinds: basis.py:29-31 (MONOMIAL, LEGENDRE) */
+enum { PGX_BASIS_MONOMIAL = 0, PGX_BASIS_LEGENDRE = 1 };
+
+/* precision modes (DESIGN.md "Precision modes" states each tolerance) */
+enum {
+    PGX_PREC_EXACT = 0, /* fp64 logits, fp64 exp/log — reference-faithful     */
+    PGX_PREC_FP64 = 1,  /* fp64 logits, fp32 (MUFU) exp of an fp64 argument   */
+    PGX_PREC_TC = 2     /* tcgen05 fp16-split logits + fp64 near-min refine   */
+};
+
+/* flags for pgx_eval / pgx_assign */
+enum {
+    PGX_WANT_GRAD = 1u,   /* objective.py:109-113 (want_grad)   */
+    PGX_WANT_ASSIGN = 2u, /* objective.py:115-119 (want_assign) */
+    PGX_DEVICE_PTRS = 4u, /* pointers are device memory; async on the stream */
+    PGX_THETA_F32 = 8u    /* theta is float32 instead of float64 */
+};
+
+/* where pgx_desc.points / pgx_desc.labels0 live */
+enum { PGX_MEM_HOST = 0, PGX_MEM_DEVICE = 1 };
+
+typedef struct {
+    int32_t dim;          /* ambient dimension: 2 (reference) or 3 (extension)  */
+    int32_t basis_kind;   /* PGX_BASIS_*                                        */
+    int32_t degree;       /* total degree d >= 0; K = C(d+dim, dim)             */
+    int32_t n_grains;     /* N >= 2 (geometry.py:94-95)                          */
+    int64_t n_points;     /* P >= 1                                             */
+    int32_t resolution;   /* M > 0: regular (2M)^dim grid generated on device
+                             (geometry.py:59-71); 0: unstructured points       */
+    int32_t precision;    /* PGX_PREC_*                                         */
+    const double* points; /* n_points x dim row-major when resolution == 0     */
+    const int64_t* labels0; /* n_points 0-based labels in [0, N)               */
+    int32_t mem;          /* PGX_MEM_HOST or PGX_MEM_DEVICE for points/labels0  */
+    int32_t device;       /* CUDA device ordinal                                */
+    void* stream;         /* cudaStream_t (NULL = legacy default stream)        */
+} pgx_desc;
+
+/* Scalar results of one evaluation (objective.EvalResult, objective.py:90-94,
+ * plus the counters the host needs). */
+typedef struct {
+    double phi;            /* Phi (+ lambda term)                              */
+    double err;            /* 1 - n_correct / P           (want_assign)        */
+    double e0;             /* mean(h_G - min h)           (want_assign)        */
+    double reserved;
+    int64_t n_points;      /* P                                                */
+    int64_t n_correct;     /* pixels whose tie-tolerant arg-min equals G       */
+    int64_t n_ambiguous;   /* pixels whose top-2 margin <= tau (1 + |min|)     */
+    int64_t n_nonfinite;   /* non-finite Phi / grad contributions seen         */
+} pgx_stats;
+
+typedef struct pgx_problem pgx_problem;
+
+int pgx_abi_version(void);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* pgx_last_error(void);
+
+/* Bytes of device workspace pgx_problem_create would allocate. */
+size_t pgx_workspace_bytes(const pgx_desc* desc);
+
+pgx_status pgx_problem_create(const pgx_desc* desc, pgx_problem** out);
+void pgx_problem_destroy(pgx_problem* problem);
+
+/* Re-targets the stream used by subsequent calls (cudaStream_t). */
+pgx_status pgx_set_stream(pgx_problem* problem, void* stream);
+
+/* One fused evaluation: Phi, grad (K x N, fp64, = -(1/(eps P)) sum_x
+ * (onehot - softmax) eta, no gauge projection) and the assignment statistics.
+ * lambda >= 0 adds -lambda/2 ||theta[:, :N-1]||^2 to Phi and
+ * -lambda theta[:, :N-1] to grad (lambda = 0 is the reference). grad_out may
+ * be NULL when PGX_WANT_GRAD is not set. */
+pgx_status pgx_eval(pgx_problem* problem, const void* theta, double eps, double lambda,
+                    uint32_t flags, double* grad_out, pgx_stats* stats_out);
+
+/* Tie-tolerant hard assignment: labels_out[p] = 1-based smallest grain index
+ * whose cost is <= min + 1e-12 (1 + |min|); margin_out (nullable) receives the
+ * top-2 cost margin; stats_out (nullable) receives n_correct / n_ambiguous. */
+pgx_status pgx_assign(pgx_problem* problem, const void* theta, uint32_t flags,
+                      int64_t* labels_out, float* margin_out, pgx_stats* stats_out);
+
+/* Number of kernel launches the last pgx_eval / pgx_assign enqueued. */
+int pgx_last_launch_count(pgx_problem* problem);
+
+/* Kernel-level timing (for bench.py's roofline): when enabled, every kernel
+ * a call enqueues is bracketed by CUDA events on the problem's stream. */
+pgx_status pgx_set_profiling(pgx_problem* problem, int enable);
+/* Number of timed kernels of the last call; name and duration (ms) of the
+ * i-th (pgx_profile_ms synchronises on its end event). */
+int pgx_profile_count(pgx_problem* problem);
+const char* pgx_profile_name(pgx_problem* problem, int i);
+float pgx_profile_ms(pgx_problem* problem, int i);
+
+/* Waits for all work enqueued on the problem's stream. */
+pgx_status pgx_synchronize(pgx_problem* problem);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PGX_H */

@@ -1,0 +1,609 @@
+// pgx_api.cu — the C ABI (include/pgx.h): problem lifetime, workspace,
+// dispatch onto the sm_100a kernels, host<->device staging, error mapping.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pgx.h"
+#include "pgx_common.cuh"
+#include "pgx_general.cuh"
+#include "pgx_grid.cuh"
+
+using namespace pgx;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+pgx_status fail(pgx_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+#define PGX_CUDA(call)                                                                 \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(PGX_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                 \
+  } while (0)
+
+#define PGX_LAUNCH_CHECK() PGX_CUDA(cudaGetLastError())
+
+int max_degree_for(int dim) { return dim == 2 ? kMaxDegree2 : kMaxDegree3; }
+
+}  // namespace
+
+struct pgx_problem {
+  int dim = 2, kind = PGX_BASIS_LEGENDRE, degree = 1, K = 3, N = 2, M = 0, prec = PGX_PREC_FP64;
+  int device = 0;
+  int64_t P = 0;
+  bool has_labels = false;
+  cudaStream_t stream = nullptr;
+  int last_launches = 0;
+
+  // device buffers owned by the problem
+  double* d_points = nullptr;
+  int32_t* d_labels = nullptr;
+  double* d_theta = nullptr;      // K x N fp64 working copy
+  void* d_theta_in = nullptr;     // host-theta staging (K x N x 8 bytes)
+  double* d_pix_m = nullptr;
+  double* d_pix_ls = nullptr;
+  int* d_fix_list = nullptr;
+  int* d_counters = nullptr;      // [0] fix_count, [1] nonfinite grad
+  long long* d_fix_correct = nullptr;
+  double* d_part_d = nullptr;
+  long long* d_part_i = nullptr;
+  double* d_part_g = nullptr;
+  double* d_grad = nullptr;       // host-mode staging
+  pgx_stats* d_stats = nullptr;   // host-mode staging
+  long long* d_labels_out = nullptr;
+  float* d_margin_out = nullptr;
+  int blocks1 = 0;   // general pass-1 blocks
+  int splits = 1;    // pass-2 point splits
+  GridPlan grid;     // regular-grid fast path plan (grid.enabled)
+  size_t bytes = 0;
+
+  // kernel-level profiling: event pairs recorded on the stream around launches
+  static constexpr int kProfMax = 32;
+  bool profiling = false;
+  cudaEvent_t prof_ev[2 * kProfMax] = {};
+  const char* prof_name[kProfMax] = {};
+  int prof_n = 0;
+  void prof_reset() { prof_n = 0; }
+  void prof_begin(const char* name) {
+    if (!profiling || prof_n >= kProfMax) return;
+    prof_name[prof_n] = name;
+    cudaEventRecord(prof_ev[2 * prof_n], stream);
+  }
+  void prof_end() {
+    if (!profiling || prof_n >= kProfMax) return;
+    cudaEventRecord(prof_ev[2 * prof_n + 1], stream);
+    ++prof_n;
+  }
+
+  template <typename T>
+  cudaError_t alloc(T** p, size_t n) {
+    bytes += n * sizeof(T);
+    return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(1, n) * sizeof(T));
+  }
+  void release() {
+    void* bufs[] = {d_points, d_labels, d_theta, d_theta_in, d_pix_m, d_pix_ls, d_fix_list,
+                    d_counters, d_fix_correct, d_part_d, d_part_i, d_part_g, d_grad, d_stats,
+                    d_labels_out, d_margin_out, grid.d_part};
+    for (void* b : bufs)
+      if (b) cudaFree(b);
+    for (cudaEvent_t& e : prof_ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+namespace {
+
+int sm_count(int device) {
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+  return n;
+}
+
+// ------------------------------------------------------------------ dispatch
+template <int DIM, int D>
+void launch_general_pass1(const EvalParams& prm, int blocks, bool eval, cudaStream_t s) {
+  if (eval)
+    k_general_pass1<DIM, D, true><<<blocks, kP1Threads, 0, s>>>(prm);
+  else
+    k_general_pass1<DIM, D, false><<<blocks, kP1Threads, 0, s>>>(prm);
+}
+template <int DIM, int D>
+void launch_general_fixup(const EvalParams& prm, int sms, cudaStream_t s) {
+  k_general_fixup<DIM, D><<<sms, 128, 0, s>>>(prm);
+}
+template <int DIM, int D>
+void launch_general_pass2(const EvalParams& prm, int N, int splits, cudaStream_t s) {
+  dim3 grid((N + kP2Threads - 1) / kP2Threads, splits);
+  k_general_pass2<DIM, D><<<grid, kP2Threads, 0, s>>>(prm);
+}
+
+#define PGX_DEG_SWITCH2(FN, ...)                 \
+  switch (pb->degree) {                          \
+    case 0: FN<2, 0>(__VA_ARGS__); break;        \
+    case 1: FN<2, 1>(__VA_ARGS__); break;        \
+    case 2: FN<2, 2>(__VA_ARGS__); break;        \
+    case 3: FN<2, 3>(__VA_ARGS__); break;        \
+    case 4: FN<2, 4>(__VA_ARGS__); break;        \
+    case 5: FN<2, 5>(__VA_ARGS__); break;        \
+    case 6: FN<2, 6>(__VA_ARGS__); break;        \
+    case 7: FN<2, 7>(__VA_ARGS__); break;        \
+    case 8: FN<2, 8>(__VA_ARGS__); break;        \
+    case 9: FN<2, 9>(__VA_ARGS__); break;        \
+    default: FN<2, 10>(__VA_ARGS__); break;      \
+  }
+#define PGX_DEG_SWITCH3(FN, ...)                 \
+  switch (pb->degree) {                          \
+    case 0: FN<3, 0>(__VA_ARGS__); break;        \
+    case 1: FN<3, 1>(__VA_ARGS__); break;        \
+    case 2: FN<3, 2>(__VA_ARGS__); break;        \
+    case 3: FN<3, 3>(__VA_ARGS__); break;        \
+    default: FN<3, 4>(__VA_ARGS__); break;       \
+  }
+#define PGX_DISPATCH(FN, ...)                                      \
+  do {                                                             \
+    if (pb->dim == 2) {                                            \
+      PGX_DEG_SWITCH2(FN, __VA_ARGS__)                             \
+    } else {                                                       \
+      PGX_DEG_SWITCH3(FN, __VA_ARGS__)                             \
+    }                                                              \
+  } while (0)
+
+EvalParams make_params(pgx_problem* pb, double eps) {
+  EvalParams prm{};
+  prm.P = pb->P;
+  prm.N = pb->N;
+  prm.M = pb->M;
+  prm.legendre = pb->kind == PGX_BASIS_LEGENDRE;
+  prm.pts = pb->d_points;
+  prm.labels = pb->has_labels ? pb->d_labels : nullptr;
+  prm.theta = pb->d_theta;
+  prm.eps = eps;
+  prm.inv_eps = 1.0 / eps;
+  prm.tau_amb = 1e-10;
+  prm.pix_m = pb->d_pix_m;
+  prm.pix_ls = pb->d_pix_ls;
+  prm.part_d = pb->d_part_d;
+  prm.part_i = pb->d_part_i;
+  prm.fix_count = pb->d_counters;
+  prm.fix_list = pb->d_fix_list;
+  prm.fix_correct = pb->d_fix_correct;
+  prm.splits = pb->splits;
+  prm.part_g = pb->d_part_g;
+  return prm;
+}
+
+// theta (host or device, f32 or f64) -> the fp64 pointer the kernels read.
+pgx_status stage_theta(pgx_problem* pb, const void* theta, uint32_t flags, const double** out,
+                       int* launches) {
+  const size_t KN = (size_t)pb->K * pb->N;
+  const bool f32 = flags & PGX_THETA_F32;
+  const bool dev = flags & PGX_DEVICE_PTRS;
+  if (!theta) return fail(PGX_ERR_INVALID_ARGUMENT, "theta must not be NULL");
+  if (dev && !f32) {
+    *out = static_cast<const double*>(theta);
+    return PGX_OK;
+  }
+  const void* src = theta;
+  if (!dev) {
+    PGX_CUDA(cudaMemcpyAsync(pb->d_theta_in, theta, KN * (f32 ? 4 : 8), cudaMemcpyHostToDevice,
+                             pb->stream));
+    src = pb->d_theta_in;
+    if (!f32) {
+      *out = static_cast<const double*>(pb->d_theta_in);
+      return PGX_OK;
+    }
+  }
+  const int blocks = (int)std::min<size_t>((KN + 255) / 256, 1024);
+  k_theta_to_f64<<<blocks, 256, 0, pb->stream>>>(src, 1, (int64_t)KN, pb->d_theta);
+  PGX_LAUNCH_CHECK();
+  ++*launches;
+  *out = pb->d_theta;
+  return PGX_OK;
+}
+
+pgx_status validate_desc(const pgx_desc* d) {
+  if (!d) return fail(PGX_ERR_INVALID_ARGUMENT, "descriptor must not be NULL");
+  if (d->dim != 2 && d->dim != 3)
+    return fail(PGX_ERR_INVALID_ARGUMENT, "dim must be 2 or 3, got %d", d->dim);
+  if (d->basis_kind != PGX_BASIS_LEGENDRE && d->basis_kind != PGX_BASIS_MONOMIAL)
+    return fail(PGX_ERR_INVALID_ARGUMENT, "unknown basis kind %d", d->basis_kind);
+  if (d->degree < 0 || d->degree > max_degree_for(d->dim))
+    return fail(PGX_ERR_INVALID_ARGUMENT, "degree %d unsupported for dim %d (max %d)", d->degree,
+                d->dim, max_degree_for(d->dim));
+  if (d->n_grains < 2)
+    return fail(PGX_ERR_INVALID_ARGUMENT, "a grain map needs at least two grains");
+  if (d->n_grains > (1 << 24))
+    return fail(PGX_ERR_INVALID_ARGUMENT, "n_grains %d too large", d->n_grains);
+  if (d->precision < PGX_PREC_EXACT || d->precision > PGX_PREC_TC)
+    return fail(PGX_ERR_INVALID_ARGUMENT, "unknown precision mode %d", d->precision);
+  if (d->resolution > 0) {
+    int64_t side = 2 * (int64_t)d->resolution;
+    int64_t expect = side * side * (d->dim == 3 ? side : 1);
+    if (d->n_points != expect)
+      return fail(PGX_ERR_INVALID_ARGUMENT, "regular grid with M=%d requires %lld points, got %lld",
+                  d->resolution, (long long)expect, (long long)d->n_points);
+  } else {
+    if (d->n_points < 1) return fail(PGX_ERR_INVALID_ARGUMENT, "a grid needs at least one point");
+    if (!d->points) return fail(PGX_ERR_INVALID_ARGUMENT, "unstructured grid needs points");
+  }
+  if (d->n_points > ((int64_t)1 << 31) - 1)
+    return fail(PGX_ERR_INVALID_ARGUMENT, "n_points too large");
+  return PGX_OK;
+}
+
+size_t workspace_estimate(const pgx_desc* d, int sms) {
+  const int64_t P = d->n_points;
+  const int K = feature_count(d->dim, d->degree);
+  const int64_t KN = (int64_t)K * d->n_grains;
+  const int64_t blocks1 = (P + kP1Threads - 1) / kP1Threads;
+  const int tiles = (d->n_grains + kP2Threads - 1) / kP2Threads;
+  const int splits = std::max(1, std::min<int>(4 * sms / tiles, (int)((P + 1023) / 1024)));
+  size_t b = 0;
+  b += (d->resolution > 0 ? 0 : (size_t)P * d->dim * 8);
+  b += (size_t)P * 4 + (size_t)KN * 8 * 3 + (size_t)P * 8 * 2 + (size_t)P * 4;
+  b += (size_t)blocks1 * (16 + 32) + (size_t)splits * KN * 8;
+  b += (size_t)P * 12;
+  b += grid_workspace_bytes(d, sms);
+  return b;
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+int pgx_abi_version(void) { return PGX_ABI_VERSION; }
+
+const char* pgx_last_error(void) { return g_last_error.c_str(); }
+
+size_t pgx_workspace_bytes(const pgx_desc* desc) {
+  if (validate_desc(desc) != PGX_OK) return 0;
+  return workspace_estimate(desc, 148);
+}
+
+pgx_status pgx_problem_create(const pgx_desc* desc, pgx_problem** out) {
+  g_last_error.clear();
+  if (!out) return fail(PGX_ERR_INVALID_ARGUMENT, "out must not be NULL");
+  *out = nullptr;
+  pgx_status st = validate_desc(desc);
+  if (st != PGX_OK) return st;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(PGX_ERR_CUDA, "no CUDA device available (the pgx hot path has no CPU fallback)");
+  PGX_CUDA(cudaSetDevice(desc->device));
+
+  pgx_problem* pb = new pgx_problem();
+  pb->dim = desc->dim;
+  pb->kind = desc->basis_kind;
+  pb->degree = desc->degree;
+  pb->K = feature_count(desc->dim, desc->degree);
+  pb->N = desc->n_grains;
+  pb->P = desc->n_points;
+  pb->M = desc->resolution;
+  pb->prec = desc->precision;
+  pb->device = desc->device;
+  pb->stream = static_cast<cudaStream_t>(desc->stream);
+  const int sms = sm_count(desc->device);
+  const int64_t P = pb->P;
+  const int64_t KN = (int64_t)pb->K * pb->N;
+  pb->blocks1 = (int)((P + kP1Threads - 1) / kP1Threads);
+  const int tiles = (pb->N + kP2Threads - 1) / kP2Threads;
+  pb->splits = std::max(1, std::min<int>(4 * sms / tiles, (int)((P + 1023) / 1024)));
+
+  cudaError_t e = cudaSuccess;
+  auto A = [&](cudaError_t r) {
+    if (e == cudaSuccess) e = r;
+  };
+  if (pb->M == 0) A(pb->alloc(&pb->d_points, (size_t)P * pb->dim));
+  A(pb->alloc(&pb->d_labels, (size_t)P));
+  A(pb->alloc(&pb->d_theta, (size_t)KN));
+  A(pb->alloc(reinterpret_cast<double**>(&pb->d_theta_in), (size_t)KN));
+  A(pb->alloc(&pb->d_pix_m, (size_t)P));
+  A(pb->alloc(&pb->d_pix_ls, (size_t)P));
+  A(pb->alloc(&pb->d_fix_list, (size_t)P));
+  A(pb->alloc(&pb->d_counters, 4));
+  A(pb->alloc(&pb->d_fix_correct, 2));
+  A(pb->alloc(&pb->d_part_d, (size_t)pb->blocks1 * 2));
+  A(pb->alloc(&pb->d_part_i, (size_t)pb->blocks1 * 4));
+  A(pb->alloc(&pb->d_part_g, (size_t)pb->splits * KN));
+  A(pb->alloc(&pb->d_grad, (size_t)KN));
+  A(pb->alloc(&pb->d_stats, 1));
+  A(pb->alloc(&pb->d_labels_out, (size_t)P));
+  A(pb->alloc(&pb->d_margin_out, (size_t)P));
+  if (e == cudaSuccess) e = grid_plan_create(pb->grid, desc, sms, pb->bytes);
+  if (e != cudaSuccess) {
+    size_t need = workspace_estimate(desc, sms);
+    pb->release();
+    delete pb;
+    cudaGetLastError();
+    if (e == cudaErrorMemoryAllocation)
+      return fail(PGX_ERR_RESOURCE,
+                  "device workspace allocation failed: needs about %zu bytes (P=%lld, K=%d, N=%d)",
+                  need, (long long)P, feature_count(desc->dim, desc->degree), desc->n_grains);
+    return fail(PGX_ERR_CUDA, "workspace allocation failed: %s", cudaGetErrorString(e));
+  }
+
+  // points
+  const bool dev_in = desc->mem == PGX_MEM_DEVICE;
+  const cudaMemcpyKind kind_in = dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if (pb->M == 0) {
+    if (!dev_in) {
+      // geometry.py:40-43: finite and strictly inside the open cube
+      for (int64_t q = 0; q < P * pb->dim; ++q) {
+        double v = desc->points[q];
+        if (!(v > -1.0 && v < 1.0)) {
+          pb->release();
+          delete pb;
+          return fail(PGX_ERR_INVALID_ARGUMENT,
+                      "grid points must be finite and lie strictly inside [-1,1]^%d", desc->dim);
+        }
+      }
+    }
+    cudaError_t c = cudaMemcpy(pb->d_points, desc->points, (size_t)P * pb->dim * 8, kind_in);
+    if (c != cudaSuccess) {
+      pb->release();
+      delete pb;
+      return fail(PGX_ERR_CUDA, "copying points failed: %s", cudaGetErrorString(c));
+    }
+  }
+  // labels: int64 0-based -> int32 on device, range-checked (geometry.py:96-97)
+  if (desc->labels0) {
+    std::vector<int64_t> host((size_t)P);
+    cudaError_t c =
+        cudaMemcpy(host.data(), desc->labels0, (size_t)P * 8,
+                   dev_in ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost);
+    if (c != cudaSuccess) {
+      pb->release();
+      delete pb;
+      return fail(PGX_ERR_CUDA, "reading labels failed: %s", cudaGetErrorString(c));
+    }
+    std::vector<int32_t> l32((size_t)P);
+    for (int64_t q = 0; q < P; ++q) {
+      int64_t v = host[(size_t)q];
+      if (v < 0 || v >= pb->N) {
+        pb->release();
+        delete pb;
+        return fail(PGX_ERR_INVALID_ARGUMENT, "labels must lie in 1..%d", pb->N);
+      }
+      l32[(size_t)q] = (int32_t)v;
+    }
+    c = cudaMemcpy(pb->d_labels, l32.data(), (size_t)P * 4, cudaMemcpyHostToDevice);
+    if (c != cudaSuccess) {
+      pb->release();
+      delete pb;
+      return fail(PGX_ERR_CUDA, "copying labels failed: %s", cudaGetErrorString(c));
+    }
+    pb->has_labels = true;
+  }
+  *out = pb;
+  return PGX_OK;
+}
+
+void pgx_problem_destroy(pgx_problem* pb) {
+  if (!pb) return;
+  cudaSetDevice(pb->device);
+  if (pb->stream) cudaStreamSynchronize(pb->stream);
+  pb->release();
+  delete pb;
+}
+
+pgx_status pgx_set_stream(pgx_problem* pb, void* stream) {
+  if (!pb) return fail(PGX_ERR_INVALID_ARGUMENT, "problem must not be NULL");
+  pb->stream = static_cast<cudaStream_t>(stream);
+  return PGX_OK;
+}
+
+int pgx_last_launch_count(pgx_problem* pb) { return pb ? pb->last_launches : 0; }
+
+pgx_status pgx_set_profiling(pgx_problem* pb, int enable) {
+  if (!pb) return fail(PGX_ERR_INVALID_ARGUMENT, "problem must not be NULL");
+  PGX_CUDA(cudaSetDevice(pb->device));
+  if (enable && !pb->prof_ev[0])
+    for (cudaEvent_t& e : pb->prof_ev) PGX_CUDA(cudaEventCreate(&e));
+  pb->profiling = enable != 0;
+  pb->prof_n = 0;
+  return PGX_OK;
+}
+
+int pgx_profile_count(pgx_problem* pb) { return pb ? pb->prof_n : 0; }
+
+const char* pgx_profile_name(pgx_problem* pb, int i) {
+  if (!pb || i < 0 || i >= pb->prof_n) return "";
+  return pb->prof_name[i];
+}
+
+float pgx_profile_ms(pgx_problem* pb, int i) {
+  if (!pb || i < 0 || i >= pb->prof_n) return -1.0f;
+  float ms = -1.0f;
+  if (cudaEventSynchronize(pb->prof_ev[2 * i + 1]) != cudaSuccess) return -1.0f;
+  if (cudaEventElapsedTime(&ms, pb->prof_ev[2 * i], pb->prof_ev[2 * i + 1]) != cudaSuccess)
+    return -1.0f;
+  return ms;
+}
+
+pgx_status pgx_synchronize(pgx_problem* pb) {
+  if (!pb) return fail(PGX_ERR_INVALID_ARGUMENT, "problem must not be NULL");
+  PGX_CUDA(cudaStreamSynchronize(pb->stream));
+  return PGX_OK;
+}
+
+pgx_status pgx_eval(pgx_problem* pb, const void* theta, double eps, double lambda, uint32_t flags,
+                    double* grad_out, pgx_stats* stats_out) {
+  g_last_error.clear();
+  if (!pb) return fail(PGX_ERR_INVALID_ARGUMENT, "problem must not be NULL");
+  if (!(eps > 0.0) || !std::isfinite(eps)) return fail(PGX_ERR_INVALID_ARGUMENT, "eps must be positive");
+  if (!(lambda >= 0.0) || !std::isfinite(lambda))
+    return fail(PGX_ERR_INVALID_ARGUMENT, "lambda must be a finite non-negative number");
+  if (!pb->has_labels)
+    return fail(PGX_ERR_INVALID_ARGUMENT, "problem was created without labels; only pgx_assign is available");
+  const bool want_grad = flags & PGX_WANT_GRAD;
+  const bool want_assign = flags & PGX_WANT_ASSIGN;
+  const bool dev = flags & PGX_DEVICE_PTRS;
+  if (want_grad && !grad_out) return fail(PGX_ERR_INVALID_ARGUMENT, "grad_out must not be NULL");
+  if (!stats_out) return fail(PGX_ERR_INVALID_ARGUMENT, "stats_out must not be NULL");
+  PGX_CUDA(cudaSetDevice(pb->device));
+  cudaStream_t s = pb->stream;
+  int launches = 0;
+  pb->prof_reset();
+  const double* theta64 = nullptr;
+  pgx_status st = stage_theta(pb, theta, flags, &theta64, &launches);
+  if (st != PGX_OK) return st;
+
+  PGX_CUDA(cudaMemsetAsync(pb->d_counters, 0, 4 * sizeof(int), s));
+  PGX_CUDA(cudaMemsetAsync(pb->d_fix_correct, 0, 2 * sizeof(long long), s));
+  EvalParams prm = make_params(pb, eps);
+  prm.theta = theta64;
+  double* grad_dst = dev ? grad_out : pb->d_grad;
+  pgx_stats* stats_dst = dev ? stats_out : pb->d_stats;
+  int blocks1 = pb->blocks1;
+
+  if (pb->grid.enabled && pb->prec != PGX_PREC_EXACT) {
+    st = grid_eval(pb->grid, prm, pb->prec, want_grad, s, &launches, &blocks1);
+    if (st != PGX_OK) return fail(st, "grid path: %s", cudaGetErrorString(cudaGetLastError()));
+    PGX_LAUNCH_CHECK();
+  } else {
+    pb->prof_begin("general_pass1");
+    PGX_DISPATCH(launch_general_pass1, prm, pb->blocks1, true, s);
+    pb->prof_end();
+    PGX_LAUNCH_CHECK();
+    pb->prof_begin("general_fixup");
+    PGX_DISPATCH(launch_general_fixup, prm, sm_count(pb->device), s);
+    pb->prof_end();
+    PGX_LAUNCH_CHECK();
+    launches += 2;
+    if (want_grad) {
+      pb->prof_begin("general_pass2");
+      PGX_DISPATCH(launch_general_pass2, prm, pb->N, pb->splits, s);
+      pb->prof_end();
+      PGX_LAUNCH_CHECK();
+      ++launches;
+    }
+  }
+  if (want_grad) {
+    ReduceParams rp{};
+    rp.K = pb->K;
+    rp.N = pb->N;
+    rp.splits = pb->grid.enabled && pb->prec != PGX_PREC_EXACT ? pb->grid.splits_out : pb->splits;
+    rp.P = pb->P;
+    rp.eps = eps;
+    rp.lambda = lambda;
+    rp.theta = theta64;
+    rp.part_g = pb->grid.enabled && pb->prec != PGX_PREC_EXACT ? pb->grid.part_out : pb->d_part_g;
+    rp.grad_out = grad_dst;
+    rp.nonfinite = pb->d_counters + 1;
+    const int64_t KN = (int64_t)pb->K * pb->N;
+    const int blocks = (int)std::min<int64_t>((KN + 255) / 256, 4 * 148);
+    pb->prof_begin("reduce_grad");
+    k_reduce_grad<<<blocks, 256, 0, s>>>(rp);
+    pb->prof_end();
+    PGX_LAUNCH_CHECK();
+    ++launches;
+  }
+  FinalParams fp{};
+  fp.blocks1 = blocks1;
+  fp.K = pb->K;
+  fp.N = pb->N;
+  fp.P = pb->P;
+  fp.eps = eps;
+  fp.lambda = lambda;
+  fp.want_assign = want_assign;
+  fp.theta = theta64;
+  fp.part_d = pb->d_part_d;
+  fp.part_i = pb->d_part_i;
+  fp.fix_correct = pb->d_fix_correct;
+  fp.nonfinite_grad = want_grad ? pb->d_counters + 1 : nullptr;
+  fp.stats_out = stats_dst;
+  pb->prof_begin("finalize");
+  k_finalize<<<1, 256, 0, s>>>(fp);
+  pb->prof_end();
+  PGX_LAUNCH_CHECK();
+  ++launches;
+  pb->last_launches = launches;
+
+  if (!dev) {
+    if (want_grad)
+      PGX_CUDA(cudaMemcpyAsync(grad_out, pb->d_grad, (size_t)pb->K * pb->N * 8,
+                               cudaMemcpyDeviceToHost, s));
+    PGX_CUDA(cudaMemcpyAsync(stats_out, pb->d_stats, sizeof(pgx_stats), cudaMemcpyDeviceToHost, s));
+    PGX_CUDA(cudaStreamSynchronize(s));
+    if (stats_out->n_nonfinite > 0)
+      return fail(PGX_ERR_NUMERICAL, "non-finite objective or gradient: phi=%g (%lld non-finite terms)",
+                  stats_out->phi, (long long)stats_out->n_nonfinite);
+  }
+  return PGX_OK;
+}
+
+pgx_status pgx_assign(pgx_problem* pb, const void* theta, uint32_t flags, int64_t* labels_out,
+                      float* margin_out, pgx_stats* stats_out) {
+  g_last_error.clear();
+  if (!pb) return fail(PGX_ERR_INVALID_ARGUMENT, "problem must not be NULL");
+  if (!labels_out) return fail(PGX_ERR_INVALID_ARGUMENT, "labels_out must not be NULL");
+  const bool dev = flags & PGX_DEVICE_PTRS;
+  PGX_CUDA(cudaSetDevice(pb->device));
+  cudaStream_t s = pb->stream;
+  int launches = 0;
+  const double* theta64 = nullptr;
+  pgx_status st = stage_theta(pb, theta, flags, &theta64, &launches);
+  if (st != PGX_OK) return st;
+  PGX_CUDA(cudaMemsetAsync(pb->d_counters, 0, 4 * sizeof(int), s));
+  PGX_CUDA(cudaMemsetAsync(pb->d_fix_correct, 0, 2 * sizeof(long long), s));
+  EvalParams prm = make_params(pb, 1.0);
+  prm.theta = theta64;
+  prm.labels_out = reinterpret_cast<long long*>(dev ? labels_out : (int64_t*)pb->d_labels_out);
+  prm.margin_out = margin_out ? (dev ? margin_out : pb->d_margin_out) : nullptr;
+  PGX_DISPATCH(launch_general_pass1, prm, pb->blocks1, false, s);
+  PGX_LAUNCH_CHECK();
+  PGX_DISPATCH(launch_general_fixup, prm, sm_count(pb->device), s);
+  PGX_LAUNCH_CHECK();
+  launches += 2;
+  pgx_stats* stats_dst = nullptr;
+  if (stats_out) {
+    FinalParams fp{};
+    fp.blocks1 = pb->blocks1;
+    fp.K = pb->K;
+    fp.N = pb->N;
+    fp.P = pb->P;
+    fp.eps = 1.0;
+    fp.want_assign = 1;
+    fp.theta = theta64;
+    fp.part_d = pb->d_part_d;
+    fp.part_i = pb->d_part_i;
+    fp.fix_correct = pb->d_fix_correct;
+    stats_dst = dev ? stats_out : pb->d_stats;
+    fp.stats_out = stats_dst;
+    k_finalize<<<1, 256, 0, s>>>(fp);
+    PGX_LAUNCH_CHECK();
+    ++launches;
+  }
+  pb->last_launches = launches;
+  if (!dev) {
+    PGX_CUDA(cudaMemcpyAsync(labels_out, pb->d_labels_out, (size_t)pb->P * 8, cudaMemcpyDeviceToHost, s));
+    if (margin_out)
+      PGX_CUDA(cudaMemcpyAsync(margin_out, pb->d_margin_out, (size_t)pb->P * 4,
+                               cudaMemcpyDeviceToHost, s));
+    if (stats_out)
+      PGX_CUDA(cudaMemcpyAsync(stats_out, pb->d_stats, sizeof(pgx_stats), cudaMemcpyDeviceToHost, s));
+    PGX_CUDA(cudaStreamSynchronize(s));
+  }
+  return PGX_OK;
+}
+
+}  // extern "C"

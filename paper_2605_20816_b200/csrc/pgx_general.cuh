@@ -1,0 +1,405 @@
+// pgx_general.cuh — the general fp64 CUDA-core path (any point list, any
+// supported basis/degree).  It is the reference-faithful restatement of
+// objective._chunk_stats (objective.py:97-120) on the device:
+//
+//   pass 1  (pixel-major, one thread per point): eta(x) in registers, theta
+//           staged through shared memory in grain chunks; fp64 logits
+//           h_i = theta_i . eta(x); online min / log-sum-exp over grains
+//           (objective.py:99-106); tie-tolerant arg-min (geometry.py:201-210)
+//           with a 2-entry candidate list and an exact re-scan fallback;
+//           per-point (min, log s) scratch for pass 2; fixed-order per-block
+//           partials of sum(ell), sum(e0), #correct, #ambiguous, #non-finite.
+//   pass 2  (grain-major, split over points): recomputes h, p = exp(z - log s),
+//           r = onehot - p and accumulates dtheta_i += r eta(x)
+//           (objective.py:109-113) into per-split partials.
+//   reduce  fixed-order fp64 reductions (objective.py:123-126,155-165).
+//
+// The regular-grid fast path (pgx_grid.cuh) and the tensor-core path reuse
+// pass-2's contract and the reduce kernels.
+#pragma once
+
+#include <math_constants.h>
+
+#include "pgx_common.cuh"
+
+namespace pgx {
+
+struct EvalParams {
+  int64_t P;
+  int N;
+  int M;          // grid resolution (0 = unstructured)
+  int legendre;   // basis kind
+  const double* __restrict__ pts;
+  const int32_t* __restrict__ labels;
+  const double* __restrict__ theta;  // K x N fp64
+  double eps;
+  double inv_eps;
+  double tau_amb;
+  // per-point scratch
+  double* pix_m;
+  double* pix_ls;
+  // pass-1 per-block partials
+  double* part_d;      // [blocks][2]: sum ell, sum e0
+  long long* part_i;   // [blocks][4]: correct, ambiguous, nonfinite, (unused)
+  int* fix_count;
+  int* fix_list;
+  long long* fix_correct;  // correct pixels discovered by the fix-up re-scan
+  // assign outputs (nullable)
+  long long* labels_out;
+  float* margin_out;
+  // pass 2
+  int splits;
+  double* part_g;  // [splits][K][N]
+};
+
+constexpr int kP1Threads = 128;
+constexpr int kP1Chunk = 64;
+constexpr int kP2Threads = 128;
+constexpr int kP2Chunk = 32;
+
+// Per-point running state of the grain scan.
+struct ScanState {
+  double m1, m2, s, hG, hb0, hb1;
+  int b0, b1, cnt;
+  bool dirty, needfix;
+  __device__ __forceinline__ void init() {
+    m1 = CUDART_INF;
+    m2 = CUDART_INF;
+    s = 0.0;
+    hG = 0.0;
+    hb0 = hb1 = 0.0;
+    b0 = b1 = -1;
+    cnt = 0;
+    dirty = needfix = false;
+  }
+};
+
+// One logit h of grain i.  LSE: online log-sum-exp in fp64 with exact exp.
+// The common case (h above the running tie threshold) only touches s and m2.
+template <bool LSE>
+__device__ __forceinline__ void scan_update(ScanState& st, double& thr, int i, double h,
+                                            double eps) {
+  if (h <= thr) {
+    if (h < st.m1) {
+      if (LSE) st.s = st.s * exp((h - st.m1) / eps) + 1.0;
+      st.m2 = st.m1;
+      st.m1 = h;
+      thr = tie_threshold(h);
+      // prune candidates that no longer lie within the tie tolerance
+      if (st.cnt > 0 && !(st.hb0 <= thr)) {
+        if (st.dirty) st.needfix = true;
+        if (st.cnt > 1 && st.hb1 <= thr) {
+          st.b0 = st.b1;
+          st.hb0 = st.hb1;
+          st.cnt = 1;
+        } else {
+          st.cnt = 0;
+        }
+      } else if (st.cnt > 1 && !(st.hb1 <= thr)) {
+        st.cnt = 1;
+      }
+    } else {
+      if (LSE) st.s += exp((st.m1 - h) / eps);
+      if (h < st.m2) st.m2 = h;
+    }
+    // h qualifies as a (tie-tolerant) minimiser; keep the two smallest indices
+    if (st.cnt == 0) {
+      st.b0 = i;
+      st.hb0 = h;
+      st.cnt = 1;
+    } else if (st.cnt == 1) {
+      st.b1 = i;
+      st.hb1 = h;
+      st.cnt = 2;
+    } else {
+      st.dirty = true;
+    }
+  } else {
+    if (LSE) st.s += exp((st.m1 - h) / eps);
+    if (h < st.m2) st.m2 = h;
+  }
+}
+
+// Fixed-order block reduction (deterministic): tree over kThreads entries.
+template <int kThreads, typename T>
+__device__ __forceinline__ T block_sum(T v, T* buf) {
+  const int tid = threadIdx.x;
+  buf[tid] = v;
+  __syncthreads();
+#pragma unroll
+  for (int off = kThreads / 2; off > 0; off >>= 1) {
+    if (tid < off) buf[tid] = buf[tid] + buf[tid + off];
+    __syncthreads();
+  }
+  T r = buf[0];
+  __syncthreads();
+  return r;
+}
+
+// ---------------------------------------------------------------- pass 1
+template <int DIM, int D, bool EVAL>
+__global__ void __launch_bounds__(kP1Threads) k_general_pass1(EvalParams prm) {
+  constexpr int K = feature_count(DIM, D);
+  __shared__ double th_s[K][kP1Chunk];
+  __shared__ double red_d[kP1Threads];
+  __shared__ long long red_i[kP1Threads];
+
+  const int tid = threadIdx.x;
+  const int64_t p = (int64_t)blockIdx.x * kP1Threads + tid;
+  const bool active = p < prm.P;
+  const int N = prm.N;
+
+  double eta[K];
+  int g = -1;
+  if (active) {
+    double x[DIM];
+    point_coords<DIM>(p, prm.M, prm.pts, x);
+    features<DIM, D>(x, prm.legendre != 0, eta);
+    if (prm.labels) g = prm.labels[p];
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k) eta[k] = 0.0;
+  }
+
+  ScanState st;
+  st.init();
+  double thr = CUDART_INF;
+  for (int c0 = 0; c0 < N; c0 += kP1Chunk) {
+    const int cn = min(kP1Chunk, N - c0);
+    __syncthreads();
+    for (int idx = tid; idx < K * kP1Chunk; idx += kP1Threads) {
+      const int k = idx / kP1Chunk, j = idx % kP1Chunk;
+      th_s[k][j] = (j < cn) ? prm.theta[(int64_t)k * N + c0 + j] : 0.0;
+    }
+    __syncthreads();
+    if (active) {
+      for (int j = 0; j < cn; ++j) {
+        double h = 0.0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) h = fma(th_s[k][j], eta[k], h);
+        const int i = c0 + j;
+        if (i == g) st.hG = h;
+        scan_update<EVAL>(st, thr, i, h, prm.eps);
+      }
+    }
+  }
+
+  double ell = 0.0, e0 = 0.0;
+  long long correct = 0, amb = 0, nonfinite = 0;
+  if (active) {
+    if (st.cnt == 0) st.needfix = true;
+    const double margin = st.m2 - st.m1;
+    amb = (margin <= prm.tau_amb * (1.0 + fabs(st.m1))) ? 1 : 0;
+    prm.pix_m[p] = st.m1;
+    if (EVAL) {
+      const double ls = log(st.s);
+      prm.pix_ls[p] = ls;
+      ell = (st.m1 - st.hG) / prm.eps - ls;  // objective.py:103,106
+      e0 = st.hG - st.m1;                    // objective.py:119
+      if (!isfinite(ell)) nonfinite = 1;
+    }
+    if (st.needfix) {
+      const int slot = atomicAdd(prm.fix_count, 1);
+      prm.fix_list[slot] = (int)p;
+    } else {
+      correct = (st.b0 == g) ? 1 : 0;
+      if (prm.labels_out) prm.labels_out[p] = st.b0 + 1;
+    }
+    if (prm.margin_out) prm.margin_out[p] = (float)margin;
+  }
+  const double s_ell = block_sum<kP1Threads>(ell, red_d);
+  const double s_e0 = block_sum<kP1Threads>(e0, red_d);
+  const long long s_cor = block_sum<kP1Threads>(correct, red_i);
+  const long long s_amb = block_sum<kP1Threads>(amb, red_i);
+  const long long s_nf = block_sum<kP1Threads>(nonfinite, red_i);
+  if (tid == 0) {
+    prm.part_d[2 * blockIdx.x + 0] = s_ell;
+    prm.part_d[2 * blockIdx.x + 1] = s_e0;
+    prm.part_i[4 * blockIdx.x + 0] = s_cor;
+    prm.part_i[4 * blockIdx.x + 1] = s_amb;
+    prm.part_i[4 * blockIdx.x + 2] = s_nf;
+    prm.part_i[4 * blockIdx.x + 3] = 0;
+  }
+}
+
+// Exact arg-min for the (rare) points whose candidate list overflowed:
+// smallest index with h <= min + tol (geometry.py:208-210).  h is recomputed
+// with the same fma order as pass 1, so it is bit-identical.
+template <int DIM, int D>
+__global__ void __launch_bounds__(128) k_general_fixup(EvalParams prm) {
+  constexpr int K = feature_count(DIM, D);
+  const int count = *prm.fix_count;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < count; t += gridDim.x * blockDim.x) {
+    const int64_t p = prm.fix_list[t];
+    double x[DIM], eta[K];
+    point_coords<DIM>(p, prm.M, prm.pts, x);
+    features<DIM, D>(x, prm.legendre != 0, eta);
+    const double thr = tie_threshold(prm.pix_m[p]);
+    int best = -1;
+    for (int i = 0; i < prm.N && best < 0; ++i) {
+      double h = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) h = fma(prm.theta[(int64_t)k * prm.N + i], eta[k], h);
+      if (h <= thr) best = i;
+    }
+    if (prm.labels_out) prm.labels_out[p] = best + 1;
+    if (prm.labels && best == prm.labels[p]) atomicAdd((unsigned long long*)prm.fix_correct, 1ull);
+  }
+}
+
+// ---------------------------------------------------------------- pass 2
+template <int DIM, int D>
+__global__ void __launch_bounds__(kP2Threads) k_general_pass2(EvalParams prm) {
+  constexpr int K = feature_count(DIM, D);
+  __shared__ double eta_s[K][kP2Chunk];
+  __shared__ double m_s[kP2Chunk], ls_s[kP2Chunk];
+  __shared__ int lab_s[kP2Chunk];
+
+  const int tid = threadIdx.x;
+  const int N = prm.N;
+  const int i = blockIdx.x * kP2Threads + tid;
+  const bool active = i < N;
+  const int y = blockIdx.y;
+  const int64_t pb = prm.P * y / prm.splits;
+  const int64_t pe = prm.P * (y + 1) / prm.splits;
+
+  double th[K], acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    th[k] = active ? prm.theta[(int64_t)k * N + i] : 0.0;
+    acc[k] = 0.0;
+  }
+  for (int64_t p0 = pb; p0 < pe; p0 += kP2Chunk) {
+    const int cn = (int)min((int64_t)kP2Chunk, pe - p0);
+    __syncthreads();
+    if (tid < cn) {
+      const int64_t p = p0 + tid;
+      double x[DIM], eta[K];
+      point_coords<DIM>(p, prm.M, prm.pts, x);
+      features<DIM, D>(x, prm.legendre != 0, eta);
+#pragma unroll
+      for (int k = 0; k < K; ++k) eta_s[k][tid] = eta[k];
+      m_s[tid] = prm.pix_m[p];
+      ls_s[tid] = prm.pix_ls[p];
+      lab_s[tid] = prm.labels[p];
+    }
+    __syncthreads();
+    if (active) {
+      for (int j = 0; j < cn; ++j) {
+        double h = 0.0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) h = fma(th[k], eta_s[k][j], h);
+        const double e = exp((m_s[j] - h) / prm.eps - ls_s[j]);
+        const double r = (lab_s[j] == i) ? 1.0 - e : -e;  // objective.py:110-112
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[k] = fma(r, eta_s[k][j], acc[k]);
+      }
+    }
+  }
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) prm.part_g[((int64_t)y * K + k) * N + i] = acc[k];
+  }
+}
+
+// ---------------------------------------------------------------- reductions
+struct ReduceParams {
+  int K, N, splits;
+  int64_t P;
+  double eps, lambda;
+  const double* theta;
+  const double* part_g;
+  double* grad_out;
+  int* nonfinite;  // counter
+};
+
+// grad = -(sum over splits, fixed order) / (eps P) - lambda theta (free columns)
+__global__ void __launch_bounds__(256) k_reduce_grad(ReduceParams prm) {
+  const int64_t KN = (int64_t)prm.K * prm.N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < KN;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int s = 0; s < prm.splits; ++s) acc += prm.part_g[s * KN + e];
+    double g = -acc / (prm.eps * (double)prm.P);  // objective.py:162
+    const int i = (int)(e % prm.N);
+    if (prm.lambda != 0.0 && i < prm.N - 1) g -= prm.lambda * prm.theta[e];
+    if (!isfinite(g)) atomicAdd(prm.nonfinite, 1);
+    prm.grad_out[e] = g;
+  }
+}
+
+struct FinalParams {
+  int blocks1;
+  int K, N;
+  int64_t P;
+  double eps, lambda;
+  int want_assign;
+  const double* theta;
+  const double* part_d;
+  const long long* part_i;
+  const long long* fix_correct;
+  const int* nonfinite_grad;
+  void* stats_out;  // pgx_stats layout
+};
+
+struct StatsDev {
+  double phi, err, e0, reserved;
+  long long n_points, n_correct, n_ambiguous, n_nonfinite;
+};
+
+__global__ void __launch_bounds__(256) k_finalize(FinalParams prm) {
+  __shared__ double rd[256];
+  __shared__ long long ri[256];
+  const int tid = threadIdx.x;
+  // fixed contiguous partition of the pass-1 partials per thread
+  const int per = (prm.blocks1 + 255) / 256;
+  const int b0 = tid * per, b1 = min(prm.blocks1, b0 + per);
+  double ell = 0.0, e0 = 0.0;
+  long long cor = 0, amb = 0, nf = 0;
+  for (int b = b0; b < b1; ++b) {
+    ell += prm.part_d[2 * b + 0];
+    e0 += prm.part_d[2 * b + 1];
+    cor += prm.part_i[4 * b + 0];
+    amb += prm.part_i[4 * b + 1];
+    nf += prm.part_i[4 * b + 2];
+  }
+  double th2 = 0.0;
+  if (prm.lambda != 0.0) {
+    const int64_t KN = (int64_t)prm.K * prm.N;
+    const int64_t per2 = (KN + 255) / 256;
+    for (int64_t e = tid * per2; e < min(KN, (tid + 1) * per2); ++e)
+      if (e % prm.N < prm.N - 1) th2 += prm.theta[e] * prm.theta[e];
+  }
+  ell = block_sum<256>(ell, rd);
+  e0 = block_sum<256>(e0, rd);
+  th2 = block_sum<256>(th2, rd);
+  cor = block_sum<256>(cor, ri);
+  amb = block_sum<256>(amb, ri);
+  nf = block_sum<256>(nf, ri);
+  if (tid == 0) {
+    StatsDev* out = reinterpret_cast<StatsDev*>(prm.stats_out);
+    const double P = (double)prm.P;
+    cor += *prm.fix_correct;
+    nf += prm.nonfinite_grad ? *prm.nonfinite_grad : 0;
+    double phi = ell / P;  // objective.py:161
+    if (prm.lambda != 0.0) phi -= 0.5 * prm.lambda * th2;
+    out->phi = phi;
+    out->err = prm.want_assign ? 1.0 - (double)cor / P : 0.0;  // objective.py:163
+    out->e0 = prm.want_assign ? e0 / P : 0.0;                  // objective.py:164
+    out->reserved = 0.0;
+    out->n_points = prm.P;
+    out->n_correct = cor;
+    out->n_ambiguous = amb;
+    out->n_nonfinite = nf + (isfinite(phi) ? 0 : 1);
+  }
+}
+
+// theta (fp32 or fp64) -> fp64 working copy
+__global__ void k_theta_to_f64(const void* __restrict__ src, int is_f32, int64_t n,
+                               double* __restrict__ dst) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = is_f32 ? (double)static_cast<const float*>(src)[e] : static_cast<const double*>(src)[e];
+}
+
+}  // namespace pgx
