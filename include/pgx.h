@@ -101,7 +101,7 @@ typedef struct {
     double phi;            /* Phi (+ lambda term)                              */
     double err;            /* 1 - n_correct / P           (want_assign)        */
     double e0;             /* mean(h_G - min h)           (want_assign)        */
-    double reserved;
+    double n_rescanned;    /* points whose arg-min needed the exact fp64 re-scan */
     int64_t n_points;      /* P                                                */
     int64_t n_correct;     /* pixels whose tie-tolerant arg-min equals G       */
     int64_t n_ambiguous;   /* pixels whose top-2 margin <= tau (1 + |min|)     */

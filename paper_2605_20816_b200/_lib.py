@@ -62,7 +62,7 @@ class PgxStats(ctypes.Structure):
         ("phi", c_double),
         ("err", c_double),
         ("e0", c_double),
-        ("reserved", c_double),
+        ("n_rescanned", c_double),
         ("n_points", c_int64),
         ("n_correct", c_int64),
         ("n_ambiguous", c_int64),

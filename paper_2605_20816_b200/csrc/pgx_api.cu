@@ -48,6 +48,7 @@ int max_degree_for(int dim) { return dim == 2 ? kMaxDegree2 : kMaxDegree3; }
 struct pgx_problem {
   int dim = 2, kind = PGX_BASIS_LEGENDRE, degree = 1, K = 3, N = 2, M = 0, prec = PGX_PREC_FP64;
   int device = 0;
+  int sms = 148;
   int64_t P = 0;
   bool has_labels = false;
   cudaStream_t stream = nullptr;
@@ -133,6 +134,10 @@ template <int DIM, int D>
 void launch_general_pass2(const EvalParams& prm, int N, int splits, cudaStream_t s) {
   dim3 grid((N + kP2Threads - 1) / kP2Threads, splits);
   k_general_pass2<DIM, D><<<grid, kP2Threads, 0, s>>>(prm);
+}
+template <int DIM, int D>
+void launch_tail(const EvalParams& prm, const TailParams& tp, int blocks, cudaStream_t s) {
+  k_tail<DIM, D><<<blocks, kTailThreads, 0, s>>>(prm, tp);
 }
 
 #define PGX_DEG_SWITCH2(FN, ...)                 \
@@ -302,6 +307,7 @@ pgx_status pgx_problem_create(const pgx_desc* desc, pgx_problem** out) {
   pb->device = desc->device;
   pb->stream = static_cast<cudaStream_t>(desc->stream);
   const int sms = sm_count(desc->device);
+  pb->sms = sms;
   const int64_t P = pb->P;
   const int64_t KN = (int64_t)pb->K * pb->N;
   pb->blocks1 = (int)((P + kP1Threads - 1) / kP1Threads);
@@ -329,6 +335,8 @@ pgx_status pgx_problem_create(const pgx_desc* desc, pgx_problem** out) {
   A(pb->alloc(&pb->d_labels_out, (size_t)P));
   A(pb->alloc(&pb->d_margin_out, (size_t)P));
   if (e == cudaSuccess) e = grid_plan_create(pb->grid, desc, sms, pb->bytes);
+  if (e == cudaSuccess) e = cudaMemset(pb->d_counters, 0, 4 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(pb->d_fix_correct, 0, 2 * sizeof(long long));
   if (e != cudaSuccess) {
     size_t need = workspace_estimate(desc, sms);
     pb->release();
@@ -467,16 +475,18 @@ pgx_status pgx_eval(pgx_problem* pb, const void* theta, double eps, double lambd
   pgx_status st = stage_theta(pb, theta, flags, &theta64, &launches);
   if (st != PGX_OK) return st;
 
-  PGX_CUDA(cudaMemsetAsync(pb->d_counters, 0, 4 * sizeof(int), s));
-  PGX_CUDA(cudaMemsetAsync(pb->d_fix_correct, 0, 2 * sizeof(long long), s));
+  // counters (fix-up list, non-finite, ticket) are zero here: zeroed at
+  // creation and re-armed by the last CTA of the tail kernel.
   EvalParams prm = make_params(pb, eps);
   prm.theta = theta64;
   double* grad_dst = dev ? grad_out : pb->d_grad;
   pgx_stats* stats_dst = dev ? stats_out : pb->d_stats;
   int blocks1 = pb->blocks1;
 
-  if (pb->grid.enabled && pb->prec != PGX_PREC_EXACT) {
-    st = grid_eval(pb->grid, prm, pb->prec, want_grad, s, &launches, &blocks1);
+  if (pb->grid.enabled) {
+    GridProf prof{pb, [](void* c, const char* n) { static_cast<pgx_problem*>(c)->prof_begin(n); },
+                  [](void* c) { static_cast<pgx_problem*>(c)->prof_end(); }};
+    st = grid_eval(pb->grid, prm, pb->prec, want_grad, s, &launches, &blocks1, prof);
     if (st != PGX_OK) return fail(st, "grid path: %s", cudaGetErrorString(cudaGetLastError()));
     PGX_LAUNCH_CHECK();
   } else {
@@ -484,11 +494,7 @@ pgx_status pgx_eval(pgx_problem* pb, const void* theta, double eps, double lambd
     PGX_DISPATCH(launch_general_pass1, prm, pb->blocks1, true, s);
     pb->prof_end();
     PGX_LAUNCH_CHECK();
-    pb->prof_begin("general_fixup");
-    PGX_DISPATCH(launch_general_fixup, prm, sm_count(pb->device), s);
-    pb->prof_end();
-    PGX_LAUNCH_CHECK();
-    launches += 2;
+    ++launches;
     if (want_grad) {
       pb->prof_begin("general_pass2");
       PGX_DISPATCH(launch_general_pass2, prm, pb->N, pb->splits, s);
@@ -497,27 +503,22 @@ pgx_status pgx_eval(pgx_problem* pb, const void* theta, double eps, double lambd
       ++launches;
     }
   }
-  if (want_grad) {
-    ReduceParams rp{};
-    rp.K = pb->K;
-    rp.N = pb->N;
-    rp.splits = pb->grid.enabled && pb->prec != PGX_PREC_EXACT ? pb->grid.splits_out : pb->splits;
-    rp.P = pb->P;
-    rp.eps = eps;
-    rp.lambda = lambda;
-    rp.theta = theta64;
-    rp.part_g = pb->grid.enabled && pb->prec != PGX_PREC_EXACT ? pb->grid.part_out : pb->d_part_g;
-    rp.grad_out = grad_dst;
-    rp.nonfinite = pb->d_counters + 1;
-    const int64_t KN = (int64_t)pb->K * pb->N;
-    const int blocks = (int)std::min<int64_t>((KN + 255) / 256, 4 * 148);
-    pb->prof_begin("reduce_grad");
-    k_reduce_grad<<<blocks, 256, 0, s>>>(rp);
-    pb->prof_end();
-    PGX_LAUNCH_CHECK();
-    ++launches;
-  }
-  FinalParams fp{};
+  TailParams tp{};
+  tp.want_grad = want_grad;
+  tp.fix_amb = pb->grid.enabled ? 1 : 0;
+  tp.ticket = reinterpret_cast<unsigned*>(pb->d_counters + 2);
+  ReduceParams& rp = tp.red;
+  rp.K = pb->K;
+  rp.N = pb->N;
+  rp.splits = pb->grid.enabled ? pb->grid.splits_out : pb->splits;
+  rp.P = pb->P;
+  rp.eps = eps;
+  rp.lambda = lambda;
+  rp.theta = theta64;
+  rp.part_g = pb->grid.enabled ? pb->grid.part_out : pb->d_part_g;
+  rp.grad_out = grad_dst;
+  rp.nonfinite = pb->d_counters + 1;
+  FinalParams& fp = tp.fin;
   fp.blocks1 = blocks1;
   fp.K = pb->K;
   fp.N = pb->N;
@@ -531,8 +532,11 @@ pgx_status pgx_eval(pgx_problem* pb, const void* theta, double eps, double lambd
   fp.fix_correct = pb->d_fix_correct;
   fp.nonfinite_grad = want_grad ? pb->d_counters + 1 : nullptr;
   fp.stats_out = stats_dst;
-  pb->prof_begin("finalize");
-  k_finalize<<<1, 256, 0, s>>>(fp);
+  const int64_t KN = (int64_t)pb->K * pb->N;
+  const int tail_blocks =
+      want_grad ? (int)std::min<int64_t>((KN + 31) / 32, 4 * pb->sms) : pb->sms;
+  pb->prof_begin("tail");
+  PGX_DISPATCH(launch_tail, prm, tp, tail_blocks, s);
   pb->prof_end();
   PGX_LAUNCH_CHECK();
   ++launches;
@@ -563,36 +567,31 @@ pgx_status pgx_assign(pgx_problem* pb, const void* theta, uint32_t flags, int64_
   const double* theta64 = nullptr;
   pgx_status st = stage_theta(pb, theta, flags, &theta64, &launches);
   if (st != PGX_OK) return st;
-  PGX_CUDA(cudaMemsetAsync(pb->d_counters, 0, 4 * sizeof(int), s));
-  PGX_CUDA(cudaMemsetAsync(pb->d_fix_correct, 0, 2 * sizeof(long long), s));
   EvalParams prm = make_params(pb, 1.0);
   prm.theta = theta64;
   prm.labels_out = reinterpret_cast<long long*>(dev ? labels_out : (int64_t*)pb->d_labels_out);
   prm.margin_out = margin_out ? (dev ? margin_out : pb->d_margin_out) : nullptr;
   PGX_DISPATCH(launch_general_pass1, prm, pb->blocks1, false, s);
   PGX_LAUNCH_CHECK();
-  PGX_DISPATCH(launch_general_fixup, prm, sm_count(pb->device), s);
+  ++launches;
+  TailParams tp{};
+  tp.want_grad = 0;
+  tp.ticket = reinterpret_cast<unsigned*>(pb->d_counters + 2);
+  FinalParams& fp = tp.fin;
+  fp.blocks1 = pb->blocks1;
+  fp.K = pb->K;
+  fp.N = pb->N;
+  fp.P = pb->P;
+  fp.eps = 1.0;
+  fp.want_assign = 1;
+  fp.theta = theta64;
+  fp.part_d = pb->d_part_d;
+  fp.part_i = pb->d_part_i;
+  fp.fix_correct = pb->d_fix_correct;
+  fp.stats_out = (stats_out && dev) ? (void*)stats_out : (void*)pb->d_stats;
+  PGX_DISPATCH(launch_tail, prm, tp, pb->sms, s);
   PGX_LAUNCH_CHECK();
-  launches += 2;
-  pgx_stats* stats_dst = nullptr;
-  if (stats_out) {
-    FinalParams fp{};
-    fp.blocks1 = pb->blocks1;
-    fp.K = pb->K;
-    fp.N = pb->N;
-    fp.P = pb->P;
-    fp.eps = 1.0;
-    fp.want_assign = 1;
-    fp.theta = theta64;
-    fp.part_d = pb->d_part_d;
-    fp.part_i = pb->d_part_i;
-    fp.fix_correct = pb->d_fix_correct;
-    stats_dst = dev ? stats_out : pb->d_stats;
-    fp.stats_out = stats_dst;
-    k_finalize<<<1, 256, 0, s>>>(fp);
-    PGX_LAUNCH_CHECK();
-    ++launches;
-  }
+  ++launches;
   pb->last_launches = launches;
   if (!dev) {
     PGX_CUDA(cudaMemcpyAsync(labels_out, pb->d_labels_out, (size_t)pb->P * 8, cudaMemcpyDeviceToHost, s));

@@ -343,7 +343,7 @@ struct FinalParams {
 };
 
 struct StatsDev {
-  double phi, err, e0, reserved;
+  double phi, err, e0, n_rescanned;
   long long n_points, n_correct, n_ambiguous, n_nonfinite;
 };
 
@@ -386,11 +386,172 @@ __global__ void __launch_bounds__(256) k_finalize(FinalParams prm) {
     out->phi = phi;
     out->err = prm.want_assign ? 1.0 - (double)cor / P : 0.0;  // objective.py:163
     out->e0 = prm.want_assign ? e0 / P : 0.0;                  // objective.py:164
-    out->reserved = 0.0;
+    out->n_rescanned = 0.0;
     out->n_points = prm.P;
     out->n_correct = cor;
     out->n_ambiguous = amb;
     out->n_nonfinite = nf + (isfinite(phi) ? 0 : 1);
+  }
+}
+
+// ---------------------------------------------------------------- fused tail
+// One launch after the passes: (1) exact arg-min re-scan of the flagged points
+// (grid-stride, rare), (2) fixed-order reduction of the per-split gradient
+// partials — 32 entries per CTA, 8 warps over interleaved splits, then a
+// fixed smem tree — with the -1/(eps P) scaling and the lambda term, (3) the
+// last CTA to finish (atomic ticket) reduces the pass-1 partials into the
+// scalars.  Every sum has a fixed order, so results are bit-reproducible.
+struct TailParams {
+  ReduceParams red;
+  FinalParams fin;
+  int want_grad;
+  int fix_amb;  // the re-scan decides the ambiguity of queued points (grid path)
+  unsigned* ticket;
+};
+
+constexpr int kTailThreads = 256;
+
+template <int DIM, int D>
+__global__ void __launch_bounds__(kTailThreads) k_tail(EvalParams e, TailParams t) {
+  constexpr int K = feature_count(DIM, D);
+  __shared__ double sred[8][33];
+  __shared__ bool last;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // (1) exact fp64 re-scan of the queued points: min and runner-up, then the
+  // smallest index within the tie tolerance (geometry.py:208-210); for the
+  // grid path it also decides the ambiguity of these points (fix_amb).
+  // One warp per queued point, lanes over grains (coalesced theta reads).
+  const int count = *e.fix_count;
+  const int nwarps = gridDim.x * (kTailThreads / 32);
+  for (int q = blockIdx.x * (kTailThreads / 32) + warp; q < count; q += nwarps) {
+    const int64_t p = e.fix_list[q];
+    double x[DIM], eta[K];
+    point_coords<DIM>(p, e.M, e.pts, x);
+    features<DIM, D>(x, e.legendre != 0, eta);
+    double m = CUDART_INF, m2 = CUDART_INF;
+    for (int i = lane; i < e.N; i += 32) {
+      double h = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) h = fma(e.theta[(int64_t)k * e.N + i], eta[k], h);
+      if (h < m) {
+        m2 = m;
+        m = h;
+      } else if (h < m2) {
+        m2 = h;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {  // merge (min, runner-up) pairs
+      const double om = __shfl_xor_sync(0xffffffffu, m, off);
+      const double om2 = __shfl_xor_sync(0xffffffffu, m2, off);
+      const double nm = fmin(m, om);
+      m2 = fmin(fmax(m, om), fmin(m2, om2));
+      m = nm;
+    }
+    const double thr = tie_threshold(m);
+    int best = 0x7fffffff;
+    for (int i = lane; i < e.N; i += 32) {
+      double h = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) h = fma(e.theta[(int64_t)k * e.N + i], eta[k], h);
+      if (h <= thr) {
+        best = i;
+        break;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, off));
+    if (best == 0x7fffffff) best = 0;
+    if (lane == 0) {
+      if (e.labels_out) e.labels_out[p] = best + 1;
+      if (e.labels && best == e.labels[p]) atomicAdd((unsigned long long*)e.fix_correct, 1ull);
+      if (t.fix_amb && (m2 - m) <= e.tau_amb * (1.0 + fabs(m)))
+        atomicAdd((unsigned long long*)e.fix_correct + 1, 1ull);
+    }
+  }
+
+  // (2) gradient: CTA b owns entries [32 b, 32 b + 32)
+  if (t.want_grad) {
+    const ReduceParams& r = t.red;
+    const int64_t KN = (int64_t)r.K * r.N;
+    for (int64_t base = (int64_t)blockIdx.x * 32; base < KN; base += (int64_t)gridDim.x * 32) {
+      const int64_t ent = base + lane;
+      double a = 0.0;
+      if (ent < KN)
+        for (int s = warp; s < r.splits; s += 8) a += r.part_g[s * KN + ent];
+      sred[warp][lane] = a;
+      __syncthreads();
+      if (warp == 0 && ent < KN) {
+        double acc = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) acc += sred[w][lane];
+        double gv = -acc / (r.eps * (double)r.P);  // objective.py:162
+        const int i = (int)(ent % r.N);
+        if (r.lambda != 0.0 && i < r.N - 1) gv -= r.lambda * r.theta[ent];
+        if (!isfinite(gv)) atomicAdd(r.nonfinite, 1);
+        r.grad_out[ent] = gv;
+      }
+      __syncthreads();
+    }
+  }
+
+  // (3) last CTA: scalars
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(t.ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const FinalParams& prm = t.fin;
+  __shared__ double rd[kTailThreads];
+  __shared__ long long ri[kTailThreads];
+  const int per = (prm.blocks1 + kTailThreads - 1) / kTailThreads;
+  const int b0 = tid * per, b1 = min(prm.blocks1, b0 + per);
+  double ell = 0.0, e0 = 0.0;
+  long long cor = 0, amb = 0, nf = 0;
+  for (int b = b0; b < b1; ++b) {
+    ell += prm.part_d[2 * b + 0];
+    e0 += prm.part_d[2 * b + 1];
+    cor += prm.part_i[4 * b + 0];
+    amb += prm.part_i[4 * b + 1];
+    nf += prm.part_i[4 * b + 2];
+  }
+  double th2 = 0.0;
+  if (prm.lambda != 0.0) {
+    const int64_t KN = (int64_t)prm.K * prm.N;
+    const int64_t per2 = (KN + kTailThreads - 1) / kTailThreads;
+    for (int64_t q = tid * per2; q < min(KN, (tid + 1) * per2); ++q)
+      if (q % prm.N < prm.N - 1) th2 += prm.theta[q] * prm.theta[q];
+  }
+  ell = block_sum<kTailThreads>(ell, rd);
+  e0 = block_sum<kTailThreads>(e0, rd);
+  th2 = block_sum<kTailThreads>(th2, rd);
+  cor = block_sum<kTailThreads>(cor, ri);
+  amb = block_sum<kTailThreads>(amb, ri);
+  nf = block_sum<kTailThreads>(nf, ri);
+  if (tid == 0) {
+    StatsDev* out = reinterpret_cast<StatsDev*>(prm.stats_out);
+    const double P = (double)prm.P;
+    cor += *(volatile long long*)prm.fix_correct;
+    amb += *((volatile long long*)prm.fix_correct + 1);
+    nf += prm.nonfinite_grad ? *(volatile int*)prm.nonfinite_grad : 0;
+    double phi = ell / P;  // objective.py:161
+    if (prm.lambda != 0.0) phi -= 0.5 * prm.lambda * th2;
+    out->phi = phi;
+    out->err = prm.want_assign ? 1.0 - (double)cor / P : 0.0;  // objective.py:163
+    out->e0 = prm.want_assign ? e0 / P : 0.0;                  // objective.py:164
+    out->n_rescanned = (double)*(volatile int*)e.fix_count;  // points re-scanned exactly
+    out->n_points = prm.P;
+    out->n_correct = cor;
+    out->n_ambiguous = amb;
+    out->n_nonfinite = nf + (isfinite(phi) ? 0 : 1);
+    // re-arm the counters for the next call (stream-ordered)
+    *e.fix_count = 0;
+    *(long long*)prm.fix_correct = 0;
+    *((long long*)prm.fix_correct + 1) = 0;
+    if (t.red.nonfinite) *t.red.nonfinite = 0;
+    *t.ticket = 0;
   }
 }
 

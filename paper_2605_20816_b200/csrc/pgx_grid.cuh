@@ -1,25 +1,195 @@
-// pgx_grid.cuh — regular-grid (separable) fast path.  Placeholder plan until
-// the separable kernels land; the general path serves every problem.
+// pgx_grid.cuh — regular-grid (separable) fp64 path: plan + dispatch.
+// Kernels: pgx_grid_pass1.cuh (min / arg-min / log-sum-exp), pgx_grid_pass2.cuh
+// (gradient contraction); shared pieces in pgx_grid_common.cuh.
 #pragma once
-#include "../../include/pgx.h"
-#include "pgx_general.cuh"
+
+#include <algorithm>
+
+#include "pgx_grid_common.cuh"
+#include "pgx_grid_pass1.cuh"
+#include "pgx_grid_pass2.cuh"
 
 namespace pgx {
 
 struct GridPlan {
   bool enabled = false;
+  int dim = 2, D = 1;
+  int R = 1, segs = 1, lines = 0, blocks1 = 0;
+  int GT = 128, gtiles = 1, splits = 1, lines_per_split = 1;
   int splits_out = 1;
   double* part_out = nullptr;
-  void* d_part = nullptr;
+  void* d_part = nullptr;  // single allocation: part_g | pix_w | pix_q
+  double* pix_w = nullptr;
+  float* pix_q = nullptr;
+  int smem2 = 0;
 };
 
-inline size_t grid_workspace_bytes(const pgx_desc*, int) { return 0; }
-inline cudaError_t grid_plan_create(GridPlan& g, const pgx_desc*, int, size_t&) {
-  g.enabled = false;
+inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
+  gp.enabled = false;
+  if (d->resolution <= 0 || d->precision == PGX_PREC_EXACT) return;
+  const int side = 2 * d->resolution;
+  if (side % 128 != 0) return;  // small grids use the general path
+  if (d->dim == 2 && d->degree > 8) return;
+  if (d->dim == 3 && d->degree > 4) return;
+  gp.enabled = true;
+  gp.dim = d->dim;
+  gp.D = d->degree;
+  gp.lines = (int)(d->n_points / side);
+  // pixels per thread: register blocking of the shared B'' loads, bounded by
+  // the register file and by the wave count (>= ~6 CTAs per SM when possible)
+  const int rmax = d->degree <= 3 ? 4 : (d->degree <= 5 ? 2 : 1);
+  int R = std::min(rmax, side / 128);
+  while (R > 1 && (int64_t)gp.lines * (side / (128 * R)) < 6 * sms) R /= 2;
+  gp.R = R;
+  gp.segs = side / (128 * gp.R);
+  gp.blocks1 = gp.lines * gp.segs;
+  const int N = d->n_grains;
+  // grains per pass-2 CTA: least padding, larger tile on ties
+  gp.GT = 128;
+  for (int gt : {64, 32})
+    if ((N + gt - 1) / gt * gt < (N + gp.GT - 1) / gp.GT * gp.GT) gp.GT = gt;
+  gp.gtiles = (N + gp.GT - 1) / gp.GT;
+  const int target = 8 * sms;
+  gp.splits = std::max(1, std::min(gp.lines, (target + gp.gtiles - 1) / gp.gtiles));
+  gp.lines_per_split = (gp.lines + gp.splits - 1) / gp.splits;
+  gp.splits = (gp.lines + gp.lines_per_split - 1) / gp.lines_per_split;
+  gp.splits_out = gp.splits;
+  const int K = feature_count(d->dim, d->degree);
+  gp.smem2 = K * kG2Threads * 8;
+}
+
+inline size_t grid_workspace_bytes(const pgx_desc* d, int sms) {
+  GridPlan gp;
+  grid_plan_shape(gp, d, sms);
+  if (!gp.enabled) return 0;
+  const int K = feature_count(d->dim, d->degree);
+  return (size_t)gp.splits * K * d->n_grains * 8 + (size_t)d->n_points * 12;
+}
+
+inline cudaError_t grid_plan_create(GridPlan& gp, const pgx_desc* d, int sms, size_t& bytes) {
+  grid_plan_shape(gp, d, sms);
+  if (!gp.enabled) return cudaSuccess;
+  const int K = feature_count(d->dim, d->degree);
+  const size_t part = (size_t)gp.splits * K * d->n_grains;
+  const size_t n = part * 8 + (size_t)d->n_points * 8 + (size_t)d->n_points * 4 + 256;
+  cudaError_t e = cudaMalloc(&gp.d_part, n);
+  if (e != cudaSuccess) return e;
+  bytes += n;
+  gp.part_out = static_cast<double*>(gp.d_part);
+  gp.pix_w = gp.part_out + part;
+  gp.pix_q = reinterpret_cast<float*>(gp.pix_w + d->n_points);
   return cudaSuccess;
 }
-inline pgx_status grid_eval(GridPlan&, const EvalParams&, int, bool, cudaStream_t, int*, int*) {
-  return PGX_ERR_CUDA;
+
+template <int DIM, int D>
+inline void grid_dispatch_pass1(const GridParams& g, int R, int blocks, cudaStream_t s) {
+  if (R == 4)
+    k_grid_pass1<DIM, D, 4><<<blocks, kG1Threads, 0, s>>>(g);
+  else if (R == 2)
+    k_grid_pass1<DIM, D, 2><<<blocks, kG1Threads, 0, s>>>(g);
+  else
+    k_grid_pass1<DIM, D, 1><<<blocks, kG1Threads, 0, s>>>(g);
+}
+
+template <int DIM, int D, int GT>
+inline void launch_grid_pass2_gt(const GridParams& g, dim3 grid, int smem, cudaStream_t s) {
+  auto kern = k_grid_pass2<DIM, D, GT>;
+  static bool configured = false;  // static + dynamic shared memory may exceed 48 KB
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    configured = true;
+  }
+  kern<<<grid, kG2Threads, smem, s>>>(g);
+}
+
+template <int DIM, int D>
+inline void grid_dispatch_pass2(const GridParams& g, int GT, dim3 grid, int smem, cudaStream_t s) {
+  if (GT == 32)
+    launch_grid_pass2_gt<DIM, D, 32>(g, grid, smem, s);
+  else if (GT == 64)
+    launch_grid_pass2_gt<DIM, D, 64>(g, grid, smem, s);
+  else
+    launch_grid_pass2_gt<DIM, D, 128>(g, grid, smem, s);
+}
+
+#define PGX_GRID_DEG(DIM_, FN, ...)              \
+  switch (gp.D) {                                \
+    case 0: FN<DIM_, 0>(__VA_ARGS__); break;     \
+    case 1: FN<DIM_, 1>(__VA_ARGS__); break;     \
+    case 2: FN<DIM_, 2>(__VA_ARGS__); break;     \
+    case 3: FN<DIM_, 3>(__VA_ARGS__); break;     \
+    case 4: FN<DIM_, 4>(__VA_ARGS__); break;     \
+    case 5: FN<DIM_, 5>(__VA_ARGS__); break;     \
+    case 6: FN<DIM_, 6>(__VA_ARGS__); break;     \
+    case 7: FN<DIM_, 7>(__VA_ARGS__); break;     \
+    default: FN<DIM_, 8>(__VA_ARGS__); break;    \
+  }
+#define PGX_GRID_DEG3(FN, ...)                   \
+  switch (gp.D) {                                \
+    case 0: FN<3, 0>(__VA_ARGS__); break;        \
+    case 1: FN<3, 1>(__VA_ARGS__); break;        \
+    case 2: FN<3, 2>(__VA_ARGS__); break;        \
+    case 3: FN<3, 3>(__VA_ARGS__); break;        \
+    default: FN<3, 4>(__VA_ARGS__); break;       \
+  }
+
+struct GridProf {
+  void* ctx;
+  void (*begin)(void*, const char*);
+  void (*end)(void*);
+};
+
+inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool want_grad,
+                            cudaStream_t s, int* launches, int* blocks1, const GridProf& prof) {
+  (void)prec;
+  GridParams g{};
+  g.P = e.P;
+  g.N = e.N;
+  g.M = e.M;
+  g.side = 2 * e.M;
+  g.legendre = e.legendre;
+  g.R = gp.R;
+  g.lines = gp.lines;
+  g.segs = gp.segs;
+  g.theta = e.theta;
+  g.labels = e.labels;
+  g.eps = e.eps;
+  g.c = 1.4426950408889634074 / e.eps;
+  g.tau_amb = e.tau_amb;
+  g.pix_m = e.pix_m;
+  g.pix_w = gp.pix_w;
+  g.pix_q = gp.pix_q;
+  g.part_d = e.part_d;
+  g.part_i = e.part_i;
+  g.fix_count = e.fix_count;
+  g.fix_list = e.fix_list;
+  g.GT = gp.GT;
+  g.lines_per_split = gp.lines_per_split;
+  g.splits = gp.splits;
+  g.part_g = gp.part_out;
+  prof.begin(prof.ctx, "grid_pass1");
+  if (gp.dim == 2) {
+    PGX_GRID_DEG(2, grid_dispatch_pass1, g, gp.R, gp.blocks1, s)
+  } else {
+    PGX_GRID_DEG3(grid_dispatch_pass1, g, gp.R, gp.blocks1, s)
+  }
+  prof.end(prof.ctx);
+  ++*launches;
+  *blocks1 = gp.blocks1;
+  if (cudaPeekAtLastError() != cudaSuccess) return PGX_ERR_CUDA;
+  if (want_grad) {
+    dim3 grid(gp.gtiles, gp.splits);
+    prof.begin(prof.ctx, "grid_pass2");
+    if (gp.dim == 2) {
+      PGX_GRID_DEG(2, grid_dispatch_pass2, g, gp.GT, grid, gp.smem2, s)
+    } else {
+      PGX_GRID_DEG3(grid_dispatch_pass2, g, gp.GT, grid, gp.smem2, s)
+    }
+    prof.end(prof.ctx);
+    ++*launches;
+    if (cudaPeekAtLastError() != cudaSuccess) return PGX_ERR_CUDA;
+  }
+  return PGX_OK;
 }
 
 }  // namespace pgx

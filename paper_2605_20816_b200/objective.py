@@ -45,6 +45,7 @@ class EvalStats(NamedTuple):
     n_correct: int
     n_ambiguous: int
     n_nonfinite: int
+    n_rescanned: int = 0
 
 
 def _basis_key(basis):
@@ -185,7 +186,7 @@ class Problem:
             _lib.check(self._lib.pgx_eval(self._h, t.ctypes.data, float(eps), float(lam), flags,
                                           _lib.as_ptr(grad), ctypes.addressof(st)))
             stats = EvalStats(st.phi, st.err, st.e0, st.n_points, st.n_correct, st.n_ambiguous,
-                              st.n_nonfinite)
+                              st.n_nonfinite, int(st.n_rescanned))
         res = EvalResult(phi=stats.phi, grad=grad,
                          err=stats.err if want_assign else None,
                          e0=stats.e0 if want_assign else None)

@@ -3,7 +3,8 @@ vectors and the CPU oracle, plus size-independent properties at full config
 sizes.  Tolerances (DESIGN.md "Precision modes"):
 
   exact : Phi rel 1e-12, grad 1e-10 x max|grad|, err/e0 exact-ish
-  fp64  : Phi rel 1e-9,  grad 1e-6 x max|grad| (fp32 MUFU exp of an fp64 argument)
+  fp64  : Phi 2e-7 (1+|Phi|), grad 2e-6 x max|grad| (fp64 logits; fp32 MUFU exp of
+          an exact fp64 argument — MUFU.EX2 itself has a measured ~-5e-8 bias)
 Labels: bit-exact except at pixels whose top-2 cost margin is <= 1e-6 (1+|min|)
 (counted and reported; the reference's own tie rule is 1e-12 (1+|min|)).
 """
@@ -18,7 +19,8 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"exact": (1e-12, 1e-10), "fp64": (1e-9, 1e-6)}
+TOL = {"exact": (1e-12, 1e-10), "fp64": (2e-7, 2e-6)}
+FP64_PHI, FP64_GRAD = TOL["fp64"]
 PRECISIONS = ["exact", "fp64"]
 
 
@@ -180,19 +182,27 @@ def test_full_config_properties(pgb, name):
     # gauge invariance (test_objective.py:236-244)
     c = rng.normal(size=(w.K, 1))
     s, _ = prob.eval(th + c, w.eps, want_assign=True)
-    assert abs(s.phi - a.phi) <= 1e-9 * (1 + abs(a.phi))
+    assert abs(s.phi - a.phi) <= FP64_PHI * (1 + abs(a.phi))
     # eps scaling (test_objective.py:246-254)
     e, _ = prob.eval(th / w.eps, 1.0, want_assign=True)
-    assert abs(e.phi - a.phi) <= 1e-9 * (1 + abs(a.phi))
+    assert abs(e.phi - a.phi) <= FP64_PHI * (1 + abs(a.phi))
     # un-projected gradient columns sum to zero
-    assert np.abs(a.grad.sum(axis=1)).max() <= 1e-9 * np.abs(a.grad).max()
+    assert np.abs(a.grad.sum(axis=1)).max() <= FP64_GRAD * np.abs(a.grad).max()
+    # separable grid path (fp64 mode) == reference-faithful general path (exact)
+    ex = pgb.Problem(w.grid, w.kind, w.degree, w.n_grains, w.labels0, precision="exact")
+    x, xs = ex.eval(th, w.eps, want_assign=True)
+    assert abs(x.phi - a.phi) <= FP64_PHI * (1 + abs(x.phi))
+    assert np.abs(x.grad - a.grad).max() <= FP64_GRAD * np.abs(x.grad).max()
+    assert abs(x.err - a.err) * len(w.labels0) <= xs.n_ambiguous
+    assert x.e0 == pytest.approx(a.e0, rel=1e-9)
+    ex.close()
     # theta = 0: Phi = -log N, grad = -(M - sum eta / N)/(eps P)
     z, _ = prob.eval(np.zeros((w.K, w.n_grains)), w.eps)
     assert z.phi == pytest.approx(-math.log(w.n_grains), abs=1e-12)
     pts = oracle.grid_points(w.M, w.dim)
     mom = oracle.label_moments(w.kind, w.degree, pts, w.labels0, w.n_grains)
     g0 = -(mom - mom.sum(axis=1, keepdims=True) / w.n_grains) / (w.eps * len(pts))
-    assert np.abs(z.grad - g0).max() <= 1e-9 * np.abs(g0).max()
+    assert np.abs(z.grad - g0).max() <= FP64_GRAD * np.abs(g0).max()
     prob.close()
 
 
@@ -271,6 +281,6 @@ def test_drop_in_with_reference_style_objects(pgb):
 
     th = gl.thetas(z)[1]
     phi = pgb.objective(T(th), D(), GM(), 0.5)
-    assert phi == pytest.approx(float(z["phi1"]), rel=1e-9)
+    assert phi == pytest.approx(float(z["phi1"]), rel=FP64_PHI)
     g = pgb.gradient(T(th), D(), GM(), 0.5)
     assert np.abs(g - z["grad1"]).max() <= 1e-6 * np.abs(z["grad1"]).max()
