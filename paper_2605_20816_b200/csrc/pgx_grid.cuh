@@ -8,13 +8,16 @@
 #include "pgx_grid_common.cuh"
 #include "pgx_grid_pass1.cuh"
 #include "pgx_grid_pass2.cuh"
+#include "pgx_tc_pass1.cuh"
 
 namespace pgx {
 
 struct GridPlan {
   bool enabled = false;
+  bool tc = false;  // PGX_PREC_TC: tensor-core pass 1
   int dim = 2, D = 1;
   int R = 1, segs = 1, lines = 0, blocks1 = 0;
+  int tcR = 1, tc_segs = 1, tc_blocks = 0;
   int GT = 128, gtiles = 1, splits = 1, lines_per_split = 1;
   int splits_out = 1;
   double* part_out = nullptr;
@@ -43,6 +46,17 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
   gp.R = R;
   gp.segs = side / (128 * gp.R);
   gp.blocks1 = gp.lines * gp.segs;
+  // tensor-core pass 1: <= 2 CTAs per SM (256 TMEM columns each); R tiles of
+  // 128 pixels share each chunk's coefficient build
+  gp.tc = d->precision == PGX_PREC_TC;
+  if (gp.tc) {
+    int tr = std::min(4, side / 128);
+    while (tr > 1 && (int64_t)gp.lines * (side / (128 * tr)) < 4 * sms) tr /= 2;
+    gp.tcR = tr;
+    gp.tc_segs = side / (128 * tr);
+    gp.tc_blocks = gp.lines * gp.tc_segs;
+    gp.blocks1 = gp.tc_blocks;
+  }
   const int N = d->n_grains;
   // grains per pass-2 CTA: least padding, larger tile on ties
   gp.GT = 128;
@@ -89,6 +103,29 @@ inline void grid_dispatch_pass1(const GridParams& g, int R, int blocks, cudaStre
     k_grid_pass1<DIM, D, 2><<<blocks, kG1Threads, 0, s>>>(g);
   else
     k_grid_pass1<DIM, D, 1><<<blocks, kG1Threads, 0, s>>>(g);
+}
+
+template <int DIM, int D, int R>
+inline void launch_tc_pass1_r(const GridParams& g, int blocks, cudaStream_t s) {
+  auto kern = k_tc_pass1<DIM, D, R>;
+  // at least 80 KB so that <= 2 CTAs (2 x 256 TMEM columns) share an SM
+  const int smem = std::max(TcP1Smem<D + 1, R>::TOTAL, 80 * 1024);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  kern<<<blocks, kTcThreads, smem, s>>>(g);
+}
+
+template <int DIM, int D>
+inline void tc_dispatch_pass1(const GridParams& g, int R, int blocks, cudaStream_t s) {
+  if (R == 4)
+    launch_tc_pass1_r<DIM, D, 4>(g, blocks, s);
+  else if (R == 2)
+    launch_tc_pass1_r<DIM, D, 2>(g, blocks, s);
+  else
+    launch_tc_pass1_r<DIM, D, 1>(g, blocks, s);
 }
 
 template <int DIM, int D, int GT>
@@ -167,13 +204,27 @@ inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool wa
   g.lines_per_split = gp.lines_per_split;
   g.splits = gp.splits;
   g.part_g = gp.part_out;
-  prof.begin(prof.ctx, "grid_pass1");
-  if (gp.dim == 2) {
-    PGX_GRID_DEG(2, grid_dispatch_pass1, g, gp.R, gp.blocks1, s)
+  if (gp.tc) {
+    g.R = gp.tcR;
+    g.segs = gp.tc_segs;
+    prof.begin(prof.ctx, "tc_pass1");
+    if (gp.dim == 2) {
+      PGX_GRID_DEG(2, tc_dispatch_pass1, g, gp.tcR, gp.tc_blocks, s)
+    } else {
+      PGX_GRID_DEG3(tc_dispatch_pass1, g, gp.tcR, gp.tc_blocks, s)
+    }
+    prof.end(prof.ctx);
+    g.R = gp.R;
+    g.segs = gp.segs;
   } else {
-    PGX_GRID_DEG3(grid_dispatch_pass1, g, gp.R, gp.blocks1, s)
+    prof.begin(prof.ctx, "grid_pass1");
+    if (gp.dim == 2) {
+      PGX_GRID_DEG(2, grid_dispatch_pass1, g, gp.R, gp.blocks1, s)
+    } else {
+      PGX_GRID_DEG3(grid_dispatch_pass1, g, gp.R, gp.blocks1, s)
+    }
+    prof.end(prof.ctx);
   }
-  prof.end(prof.ctx);
   ++*launches;
   *blocks1 = gp.blocks1;
   if (cudaPeekAtLastError() != cudaSuccess) return PGX_ERR_CUDA;
