@@ -9,6 +9,7 @@
 #include "pgx_grid_pass1.cuh"
 #include "pgx_grid_pass2.cuh"
 #include "pgx_tc_pass1.cuh"
+#include "pgx_tc_pass2.cuh"
 
 namespace pgx {
 
@@ -18,6 +19,8 @@ struct GridPlan {
   int dim = 2, D = 1;
   int R = 1, segs = 1, lines = 0, blocks1 = 0;
   int tcR = 1, tc_segs = 1, tc_blocks = 0;
+  int tc2_gtiles = 0, tc2_lps = 1, tc2_splits = 0;  // tensor-core pass 2 (0 = CUDA-core pass 2)
+  int part_splits = 0;                             // allocated split slots of part_g
   int GT = 128, gtiles = 1, splits = 1, lines_per_split = 1;
   int splits_out = 1;
   double* part_out = nullptr;
@@ -50,7 +53,8 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
   // 128 pixels share each chunk's coefficient build
   gp.tc = d->precision == PGX_PREC_TC;
   if (gp.tc) {
-    int tr = std::min(4, side / 128);
+    // shared memory per CTA must stay <= ~56 KB for 4 CTAs per SM
+    int tr = std::min(tc_ksteps(d->degree + 1) == 1 ? 4 : 2, side / 128);
     while (tr > 1 && (int64_t)gp.lines * (side / (128 * tr)) < 4 * sms) tr /= 2;
     gp.tcR = tr;
     gp.tc_segs = side / (128 * tr);
@@ -70,6 +74,15 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
   gp.splits_out = gp.splits;
   const int K = feature_count(d->dim, d->degree);
   gp.smem2 = K * kG2Threads * 8;
+  if (gp.tc && side % kTc2Px == 0) {
+    // tensor-core pass 2: 128-grain tiles x line ranges, 4 CTAs per SM
+    gp.tc2_gtiles = (N + kTc2Threads - 1) / kTc2Threads;
+    int sp = std::max(1, std::min(gp.lines, (8 * sms + gp.tc2_gtiles - 1) / gp.tc2_gtiles));
+    gp.tc2_lps = (gp.lines + sp - 1) / sp;
+    gp.tc2_splits = (gp.lines + gp.tc2_lps - 1) / gp.tc2_lps;
+    gp.splits_out = gp.tc2_splits;
+    gp.part_splits = std::max(gp.splits, gp.tc2_splits);
+  }
 }
 
 inline size_t grid_workspace_bytes(const pgx_desc* d, int sms) {
@@ -77,14 +90,14 @@ inline size_t grid_workspace_bytes(const pgx_desc* d, int sms) {
   grid_plan_shape(gp, d, sms);
   if (!gp.enabled) return 0;
   const int K = feature_count(d->dim, d->degree);
-  return (size_t)gp.splits * K * d->n_grains * 8 + (size_t)d->n_points * 12;
+  return (size_t)std::max(gp.splits, gp.part_splits) * K * d->n_grains * 8 + (size_t)d->n_points * 12;
 }
 
 inline cudaError_t grid_plan_create(GridPlan& gp, const pgx_desc* d, int sms, size_t& bytes) {
   grid_plan_shape(gp, d, sms);
   if (!gp.enabled) return cudaSuccess;
   const int K = feature_count(d->dim, d->degree);
-  const size_t part = (size_t)gp.splits * K * d->n_grains;
+  const size_t part = (size_t)std::max(gp.splits, gp.part_splits) * K * d->n_grains;
   const size_t n = part * 8 + (size_t)d->n_points * 8 + (size_t)d->n_points * 4 + 256;
   cudaError_t e = cudaMalloc(&gp.d_part, n);
   if (e != cudaSuccess) return e;
@@ -108,8 +121,8 @@ inline void grid_dispatch_pass1(const GridParams& g, int R, int blocks, cudaStre
 template <int DIM, int D, int R>
 inline void launch_tc_pass1_r(const GridParams& g, int blocks, cudaStream_t s) {
   auto kern = k_tc_pass1<DIM, D, R>;
-  // at least 80 KB so that <= 2 CTAs (2 x 256 TMEM columns) share an SM
-  const int smem = std::max(TcP1Smem<D + 1, R>::TOTAL, 80 * 1024);
+  // padded so that <= 4 CTAs (4 x 128 TMEM columns) share an SM
+  const int smem = std::max(TcP1Smem<D + 1, R>::TOTAL, kTcMinSmem);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -126,6 +139,18 @@ inline void tc_dispatch_pass1(const GridParams& g, int R, int blocks, cudaStream
     launch_tc_pass1_r<DIM, D, 2>(g, blocks, s);
   else
     launch_tc_pass1_r<DIM, D, 1>(g, blocks, s);
+}
+
+template <int DIM, int D>
+inline void tc_dispatch_pass2(const GridParams& g, dim3 grid, cudaStream_t s) {
+  auto kern = k_tc_pass2<DIM, D>;
+  const int smem = std::max(TcP2Smem<D + 1>::TOTAL, kTcMinSmem);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  kern<<<grid, kTc2Threads, smem, s>>>(g);
 }
 
 template <int DIM, int D, int GT>
@@ -228,7 +253,20 @@ inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool wa
   ++*launches;
   *blocks1 = gp.blocks1;
   if (cudaPeekAtLastError() != cudaSuccess) return PGX_ERR_CUDA;
-  if (want_grad) {
+  if (want_grad && gp.tc && gp.tc2_splits > 0) {
+    dim3 grid(gp.tc2_gtiles, gp.tc2_splits);
+    g.lines_per_split = gp.tc2_lps;
+    g.splits = gp.tc2_splits;
+    prof.begin(prof.ctx, "tc_pass2");
+    if (gp.dim == 2) {
+      PGX_GRID_DEG(2, tc_dispatch_pass2, g, grid, s)
+    } else {
+      PGX_GRID_DEG3(tc_dispatch_pass2, g, grid, s)
+    }
+    prof.end(prof.ctx);
+    ++*launches;
+    if (cudaPeekAtLastError() != cudaSuccess) return PGX_ERR_CUDA;
+  } else if (want_grad) {
     dim3 grid(gp.gtiles, gp.splits);
     prof.begin(prof.ctx, "grid_pass2");
     if (gp.dim == 2) {

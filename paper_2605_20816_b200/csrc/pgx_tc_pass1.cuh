@@ -24,8 +24,9 @@
 namespace pgx {
 
 constexpr int kTcThreads = 128;
-constexpr int kTcChunk = 256;     // grains per chunk (UMMA N)
-constexpr int kTcTmemCols = 256;  // one fp32 accumulator tile
+constexpr int kTcChunk = 128;     // grains per chunk (UMMA N)
+constexpr int kTcTmemCols = 128;  // one fp32 accumulator tile: 4 CTAs share an SM's TMEM
+constexpr int kTcMinSmem = 46 * 1024;  // keeps residency at <= 4 CTAs per SM
 
 // exact per-pixel state for near-minimal logits (shared memory)
 struct TcRare {
@@ -84,7 +85,7 @@ struct TcP1Smem {
 };
 
 template <int DIM, int D, int R>
-__global__ void __launch_bounds__(kTcThreads, 1) k_tc_pass1(GridParams g) {
+__global__ void __launch_bounds__(kTcThreads, 4) k_tc_pass1(GridParams g) {
   constexpr int J = D + 1;
   constexpr int K = feature_count(DIM, D);
   using L = TcP1Smem<J, R>;
@@ -278,13 +279,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_pass1(GridParams g) {
         const bool full = cb + 32 <= cn;
         const bool lab_here = (unsigned)(labc - cb) < 32u;
         bool cand = false;
-        float s = 0.0f;
+        float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // 4 independent FADD chains
         if (full && !__any_sync(0xffffffffu, lab_here)) {
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
             const float a = fmaf(v[q], inv, -ref[r]);
             cand |= a <= athr[r];
-            s += ex2_approx(-a);
+            s4[q & 3] += ex2_approx(-a);
           }
         } else {
 #pragma unroll
@@ -293,16 +294,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_pass1(GridParams g) {
             const bool ok = cb + q < cn;
             cand |= ok && a <= athr[r];
             const float e = ex2_approx(-a);
-            s += (ok && cb + q != labc) ? e : 0.0f;
+            s4[q & 3] += (ok && cb + q != labc) ? e : 0.0f;
           }
         }
-        sx64[r] += (double)s;
+        sx64[r] += (double)((s4[0] + s4[1]) + (s4[2] + s4[3]));
         if (__any_sync(0xffffffffu, cand)) {
           if (cand) {  // exact fp64 re-evaluation of the near-minimal logits
             const int col = seg * kTcThreads * R + kTcThreads * r + tid;
             double u[J];
             axis_table<D>(axis_coord(col, g.M), g.legendre != 0, u);
             TcRare& st = rare[r * kTcThreads + tid];
+#pragma unroll
             for (int q = 0; q < 32; ++q) {
               const float a = fmaf(v[q], inv, -ref[r]);
               if (cb + q < cn && a <= athr[r])
