@@ -222,29 +222,35 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_tc_pass1(GridParams g) {
   const unsigned trow = tmem + ((unsigned)(warp * 32) << 16);
 
   // ---------------------------------------------------------------- sweep A
+  // Per-tile state lives in small arrays indexed by the (rolled) tile loop:
+  // a few local-memory accesses per tile instead of R copies of the epilogue
+  // code (the unrolled version thrashed the instruction cache).
   float mt[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) mt[r] = CUDART_INF_F;
   for (int c0 = 0; c0 < N; c0 += kTcChunk) {
     const int cn = min(kTcChunk, N - c0);
     const float inv = build_chunk(c0, cn);
-#pragma unroll
+#pragma unroll 1
     for (int r = 0; r < R; ++r) {
       mma_tile(r);
-      float mr = CUDART_INF_F;
+      float m0 = CUDART_INF_F, m1 = CUDART_INF_F;
       for (int cb = 0; cb < cn; cb += 32) {
         float v[32];
         tmem_ld32(trow + cb, v);
         if (cb + 32 <= cn) {
 #pragma unroll
-          for (int q = 0; q < 32; ++q) mr = fminf(mr, v[q]);
+          for (int q = 0; q < 32; q += 2) {
+            m0 = fminf(m0, v[q]);
+            m1 = fminf(m1, v[q + 1]);
+          }
         } else {
 #pragma unroll
           for (int q = 0; q < 32; ++q)
-            if (cb + q < cn) mr = fminf(mr, v[q]);
+            if (cb + q < cn) m0 = fminf(m0, v[q]);
         }
       }
-      mt[r] = fminf(mt[r], mr * inv);
+      mt[r] = fminf(mt[r], fminf(m0, m1) * inv);
       tc_fence_before();
       __syncthreads();
       tc_fence_after();
@@ -269,10 +275,12 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_tc_pass1(GridParams g) {
   for (int c0 = 0; c0 < N; c0 += kTcChunk) {
     const int cn = min(kTcChunk, N - c0);
     const float inv = build_chunk(c0, cn);
-#pragma unroll
+#pragma unroll 1
     for (int r = 0; r < R; ++r) {
       mma_tile(r);
       const int labc = lab[r] - c0;
+      const float refr = ref[r], athrr = athr[r];
+      double sxr = sx64[r];
       for (int cb = 0; cb < cn; cb += 32) {
         float v[32];
         tmem_ld32(trow + cb, v);
@@ -283,36 +291,43 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_tc_pass1(GridParams g) {
         if (full && !__any_sync(0xffffffffu, lab_here)) {
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
-            const float a = fmaf(v[q], inv, -ref[r]);
-            cand |= a <= athr[r];
+            const float a = fmaf(v[q], inv, -refr);
+            cand |= a <= athrr;
             s4[q & 3] += ex2_approx(-a);
           }
         } else {
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
-            const float a = fmaf(v[q], inv, -ref[r]);
+            const float a = fmaf(v[q], inv, -refr);
             const bool ok = cb + q < cn;
-            cand |= ok && a <= athr[r];
+            cand |= ok && a <= athrr;
             const float e = ex2_approx(-a);
             s4[q & 3] += (ok && cb + q != labc) ? e : 0.0f;
           }
         }
-        sx64[r] += (double)((s4[0] + s4[1]) + (s4[2] + s4[3]));
+        sxr += (double)((s4[0] + s4[1]) + (s4[2] + s4[3]));
         if (__any_sync(0xffffffffu, cand)) {
-          if (cand) {  // exact fp64 re-evaluation of the near-minimal logits
+          // exact fp64 re-evaluation of the near-minimal logits: collect the
+          // candidate columns as a bit mask (static register indices), then
+          // walk the set bits
+          unsigned cm = 0u;
+#pragma unroll
+          for (int q = 0; q < 32; ++q)
+            if (fmaf(v[q], inv, -refr) <= athrr && cb + q < cn) cm |= 1u << q;
+          if (cm) {
             const int col = seg * kTcThreads * R + kTcThreads * r + tid;
             double u[J];
             axis_table<D>(axis_coord(col, g.M), g.legendre != 0, u);
             TcRare& st = rare[r * kTcThreads + tid];
-#pragma unroll
-            for (int q = 0; q < 32; ++q) {
-              const float a = fmaf(v[q], inv, -ref[r]);
-              if (cb + q < cn && a <= athr[r])
-                tc_rare_update(st, c0 + cb + q, eval_line<J>(Bd_s + (cb + q) * J, u), c);
+            while (cm) {
+              const int q = __ffs(cm) - 1;
+              cm &= cm - 1u;
+              tc_rare_update(st, c0 + cb + q, eval_line<J>(Bd_s + (cb + q) * J, u), c);
             }
           }
         }
       }
+      sx64[r] = sxr;
       tc_fence_before();
       __syncthreads();
       tc_fence_after();

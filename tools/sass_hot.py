@@ -30,3 +30,7 @@ print("--- hottest instructions")
 rows.sort(key=lambda r: -int(r["Instructions Executed"] or 0))
 for r in rows[:top]:
     print(f'{r["Address"][-5:]} {int(r["Instructions Executed"]):10d} {r["Warp Stall Sampling (All Samples)"]:>6s}  {r["Source"].strip()[:90]}')
+print("--- most stalled instructions")
+rows.sort(key=lambda r: -int(r["Warp Stall Sampling (All Samples)"] or 0))
+for r in rows[:25]:
+    print(f'{r["Address"][-5:]} {int(r["Instructions Executed"]):10d} {r["Warp Stall Sampling (All Samples)"]:>6s}  {r["Source"].strip()[:90]}')
