@@ -136,6 +136,12 @@ def max_over_ranks(value: float, world: int, device) -> float:
     return float(t.item())
 
 
+def replica_value(world: int, steps: int, units_per_step: int, t_max: float) -> float:
+    """Whole-job throughput of N independent replicas: every rank processed
+    ``steps`` x ``units_per_step`` units; the job time is the slowest rank's."""
+    return world * steps * units_per_step / t_max
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
@@ -275,7 +281,7 @@ def run_ours(args):
         step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     t_rank = sum(step_ms) / 1000.0
     t_max = max_over_ranks(t_rank, world, dev)
-    value = world * args.steps * P * N / t_max
+    value = replica_value(world, args.steps, P * N, t_max)
     stats = stats_d.cpu().numpy()
 
     # ---- kernel-level timing (dominant kernel) with CUDA events, same stream
@@ -317,7 +323,7 @@ def run_ours(args):
             e.synchronize()
             e_ms.append(s.elapsed_time(e))
     t_e2e = max_over_ranks(sum(e_ms) / 1000.0, world, dev)
-    e2e_value = world * args.steps * P * N / t_e2e
+    e2e_value = replica_value(world, args.steps, P * N, t_e2e)
     h2d = K * N * (4 if f32 else 8)
     d2h = K * N * 8 + 64
 

@@ -5,6 +5,8 @@ sizes.  Tolerances (DESIGN.md "Precision modes"):
   exact : Phi rel 1e-12, grad 1e-10 x max|grad|, err/e0 exact-ish
   fp64  : Phi 2e-7 (1+|Phi|), grad 2e-6 x max|grad| (fp64 logits; fp32 MUFU exp of
           an exact fp64 argument — MUFU.EX2 itself has a measured ~-5e-8 bias)
+  tc    : Phi 1e-6 (1+|Phi|), grad 1e-5 x max|grad| (tcgen05 logits from a 3-product
+          fp16 split with fp32 accumulation; near-minimal logits re-evaluated in fp64)
 Labels: bit-exact except at pixels whose top-2 cost margin is <= 1e-6 (1+|min|)
 (counted and reported; the reference's own tie rule is 1e-12 (1+|min|)).
 """
@@ -19,9 +21,9 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"exact": (1e-12, 1e-10), "fp64": (2e-7, 2e-6)}
+TOL = {"exact": (1e-12, 1e-10), "fp64": (2e-7, 2e-6), "tc": (1e-6, 1e-5)}
 FP64_PHI, FP64_GRAD = TOL["fp64"]
-PRECISIONS = ["exact", "fp64"]
+PRECISIONS = ["exact", "fp64", "tc"]
 
 
 @pytest.fixture(scope="module")
@@ -165,6 +167,33 @@ def test_tie_semantics(pgb):
     assert not np.any(lab == 4)  # duplicated later column never wins
     tie = np.tile(rng.normal(size=(6, 1)), (1, 4))
     assert np.all(pgb.hard_assign(pgb.ParamMatrix(tie, basis), basis, grid) == 1)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_full_size_modes_against_exact(pgb, name):
+    """Every BASELINE config at full size: the fast modes (fp64 grid path,
+    tcgen05 path) against the reference-faithful exact mode (itself pinned to
+    the oracle / golden vectors above), at the bench theta and a N(0,1) theta."""
+    from paper_2605_20816_b200 import configs
+
+    w = configs.make(name, labeler="gpu")
+    rng = np.random.default_rng(21)
+    thetas = [np.asarray(w.theta_bench, dtype=np.float64), rng.normal(size=(w.K, w.n_grains))]
+    probs = {m: pgb.Problem(w.grid, w.kind, w.degree, w.n_grains, w.labels0, precision=m)
+             for m in ("exact", "fp64", "tc")}
+    for th in thetas:
+        ref, rs = probs["exact"].eval(th, w.eps, lam=w.lam, want_assign=True)
+        for mode in ("fp64", "tc"):
+            res, st = probs[mode].eval(th, w.eps, lam=w.lam, want_assign=True)
+            tphi, tgrad = TOL[mode]
+            assert abs(res.phi - ref.phi) <= tphi * (1 + abs(ref.phi)), (mode, res.phi, ref.phi)
+            assert np.abs(res.grad - ref.grad).max() <= tgrad * np.abs(ref.grad).max(), mode
+            assert abs(res.err - ref.err) * w.n_points <= rs.n_ambiguous, mode
+            assert res.e0 == pytest.approx(ref.e0, rel=1e-9, abs=1e-12), mode
+            again, _ = probs[mode].eval(th, w.eps, lam=w.lam, want_assign=True)
+            assert again.phi == res.phi and np.array_equal(again.grad, res.grad)  # bit-reproducible
+    for p in probs.values():
+        p.close()
 
 
 @pytest.mark.parametrize("name", ["c1", "c2"])
