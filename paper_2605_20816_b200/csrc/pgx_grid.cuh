@@ -21,6 +21,11 @@ struct GridPlan {
   int tcR = 1, tc_segs = 1, tc_blocks = 0;
   int tc2_gtiles = 0, tc2_lps = 1, tc2_splits = 0;  // tensor-core pass 2 (0 = CUDA-core pass 2)
   int part_splits = 0;                             // allocated split slots of part_g
+  int tc_nchunks = 0;                              // 128-grain chunks (pgx_tc_coeffs.cuh)
+  void* d_tc = nullptr;                            // coef | img | meta
+  double* tc_coef = nullptr;
+  unsigned char* tc_img = nullptr;
+  int2* tc_meta = nullptr;
   int GT = 128, gtiles = 1, splits = 1, lines_per_split = 1;
   int splits_out = 1;
   double* part_out = nullptr;
@@ -105,6 +110,20 @@ inline cudaError_t grid_plan_create(GridPlan& gp, const pgx_desc* d, int sms, si
   gp.part_out = static_cast<double*>(gp.d_part);
   gp.pix_w = gp.part_out + part;
   gp.pix_q = reinterpret_cast<float*>(gp.pix_w + d->n_points);
+  if (gp.tc) {
+    const int J = d->degree + 1;
+    gp.tc_nchunks = (d->n_grains + kTcCoefChunk - 1) / kTcCoefChunk;
+    const size_t ncoef = (size_t)gp.lines * d->n_grains * J;
+    const size_t nimg = (size_t)gp.lines * gp.tc_nchunks * tc_ksteps(J) * kTcCoefChunk * 32;
+    const size_t nmeta = (size_t)gp.lines * gp.tc_nchunks;
+    const size_t tb = ncoef * 8 + nimg + nmeta * 8 + 256;
+    e = cudaMalloc(&gp.d_tc, tb);
+    if (e != cudaSuccess) return e;
+    bytes += tb;
+    gp.tc_coef = static_cast<double*>(gp.d_tc);
+    gp.tc_img = reinterpret_cast<unsigned char*>(gp.tc_coef + ncoef);
+    gp.tc_meta = reinterpret_cast<int2*>(gp.tc_img + nimg);
+  }
   return cudaSuccess;
 }
 
@@ -139,6 +158,14 @@ inline void tc_dispatch_pass1(const GridParams& g, int R, int blocks, cudaStream
     launch_tc_pass1_r<DIM, D, 2>(g, blocks, s);
   else
     launch_tc_pass1_r<DIM, D, 1>(g, blocks, s);
+}
+
+template <int DIM, int D>
+inline void tc_dispatch_coeffs(const GridParams& g, const GridPlan& gp, cudaStream_t s) {
+  dim3 grid(gp.tc_nchunks, gp.lines);
+  k_tc_coeffs<DIM, D><<<grid, kTcCoefChunk, 0, s>>>(g, gp.tc_coef, gp.tc_img,
+                                                    reinterpret_cast<TcCoefMeta*>(gp.tc_meta),
+                                                    gp.tc_nchunks);
 }
 
 template <int DIM, int D>
@@ -229,7 +256,19 @@ inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool wa
   g.lines_per_split = gp.lines_per_split;
   g.splits = gp.splits;
   g.part_g = gp.part_out;
+  g.tc_coef = gp.tc_coef;
+  g.tc_img = gp.tc_img;
+  g.tc_meta = gp.tc_meta;
+  g.tc_nchunks = gp.tc_nchunks;
   if (gp.tc) {
+    prof.begin(prof.ctx, "tc_coeffs");
+    if (gp.dim == 2) {
+      PGX_GRID_DEG(2, tc_dispatch_coeffs, g, gp, s)
+    } else {
+      PGX_GRID_DEG3(tc_dispatch_coeffs, g, gp, s)
+    }
+    prof.end(prof.ctx);
+    ++*launches;
     g.R = gp.tcR;
     g.segs = gp.tc_segs;
     prof.begin(prof.ctx, "tc_pass1");

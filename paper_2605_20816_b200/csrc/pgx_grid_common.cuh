@@ -100,6 +100,11 @@ struct GridParams {
   int lines_per_split;
   int splits;
   double* part_g;  // [splits][K][N]
+  // tensor-core path: per-line coefficient tables (pgx_tc_coeffs.cuh)
+  const double* tc_coef;        // [lines][N][J] exact B''
+  const unsigned char* tc_img;  // [lines][chunks] UMMA operand images
+  const int2* tc_meta;          // [lines][chunks] {sB, bnorm bits}
+  int tc_nchunks;
 };
 
 // Per-line factors: lc[k] = prod over the non-fast axes of u_axis[alpha]

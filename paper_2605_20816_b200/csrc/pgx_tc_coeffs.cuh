@@ -1,0 +1,115 @@
+// pgx_tc_coeffs.cuh — once per evaluation, the per-line grain coefficients of
+// the tensor-core path, shared by every CTA that touches the line:
+//
+//   coef[line][i][j]   exact fp64 B''_{j,i}(line) (c-scaled), for the fp64
+//                      re-evaluation of near-minimal logits and the label term;
+//   img[line][chunk]   the UMMA operand image of 128 grains: K-major
+//                      SWIZZLE_NONE slabs, K pattern [hi, lo, hi] of the
+//                      2^sB-scaled fp16 split (pass-1 B operand, pass-2 A);
+//   meta[line][chunk]  {sB, max_i sum_j |B''_{j,i}|}.
+//
+// Without it every pass-1 CTA rebuilt each chunk twice (sweeps A and B) and
+// every pass-2 CTA rebuilt its tile per line: K fp64 FMAs + K loads per grain,
+// ~30% of pass-1 instructions at c5.
+#pragma once
+
+#include "pgx_grid_common.cuh"
+#include "pgx_tc_common.cuh"
+
+namespace pgx {
+
+constexpr int kTcCoefChunk = 128;  // grains per image chunk (= pass-1 UMMA N = pass-2 M)
+
+struct TcCoefMeta {
+  int sB;       // fp16 scale exponent of the chunk
+  float bnorm;  // max over the chunk's grains of sum_j |B''_j|
+};
+
+template <int J>
+__host__ __device__ constexpr int tc_img_bytes() {
+  return tc_ksteps(J) * kTcCoefChunk * 32;
+}
+
+template <int DIM, int D>
+__global__ void __launch_bounds__(kTcCoefChunk) k_tc_coeffs(GridParams g, double* __restrict__ coef,
+                                                            unsigned char* __restrict__ img,
+                                                            TcCoefMeta* __restrict__ meta,
+                                                            int nchunks) {
+  constexpr int J = D + 1;
+  constexpr int K = feature_count(DIM, D);
+  constexpr int KS = tc_ksteps(J);
+  __shared__ double lc[K];
+  __shared__ unsigned s_max, s_b1;
+  const int tid = threadIdx.x;
+  const int chunk = blockIdx.x;
+  const int64_t line = blockIdx.y;
+  const int i = chunk * kTcCoefChunk + tid;
+  if (tid == 0) {
+    double lcr[K];
+    line_factors<DIM, D>(line, g, lcr);
+#pragma unroll
+    for (int k = 0; k < K; ++k) lc[k] = lcr[k];
+    s_max = 0u;
+    s_b1 = 0u;
+  }
+  __syncthreads();
+  double B[J];
+  if (i < g.N) {
+    line_coeffs<DIM, D>(g.theta, g.N, i, lc, g.c, B);
+    double* out = coef + (line * g.N + i) * J;
+#pragma unroll
+    for (int j = 0; j < J; ++j) out[j] = B[j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < J; ++j) B[j] = 0.0;
+  }
+  float bm = 0.0f, b1 = 0.0f;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    bm = fmaxf(bm, (float)fabs(B[j]));
+    b1 += (float)fabs(B[j]);
+  }
+  // non-finite coefficients poison the scale; the passes then flag the pixels
+  atomicMax(&s_max, __float_as_uint(isfinite(bm) ? bm : CUDART_INF_F));
+  atomicMax(&s_b1, __float_as_uint(isfinite(b1) ? b1 * 1.0000005f : CUDART_INF_F));
+  __syncthreads();
+  const float chmax = __uint_as_float(s_max);
+  const int sB = chmax > 0.0f && chmax < 3e38f ? 13 - ilogbf(chmax) : 0;
+  const double scl = ldexp(1.0, sB);
+  __half hi[J], lo[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) split_f16(B[j] * scl, hi[j], lo[j]);
+  unsigned char* dst = img + (line * nchunks + chunk) * (int64_t)tc_img_bytes<J>();
+  // row tid: 16 K-elements per slab = two 16-byte core-matrix rows
+#pragma unroll
+  for (int s = 0; s < KS; ++s) {
+    __half row[16];
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      const int k = s * 16 + kk;
+      const int b = k / J, j = k % J;
+      row[kk] = k < 3 * J ? (b == 1 ? lo[j] : hi[j]) : __float2half(0.0f);
+    }
+    unsigned char* slab = dst + s * (kTcCoefChunk * 32);
+    *reinterpret_cast<uint4*>(slab + slab_off(tid, 0)) = *reinterpret_cast<const uint4*>(row);
+    *reinterpret_cast<uint4*>(slab + slab_off(tid, 8)) = *reinterpret_cast<const uint4*>(row + 8);
+  }
+  if (tid == 0) {
+    TcCoefMeta m;
+    m.sB = sB;
+    m.bnorm = __uint_as_float(s_b1);
+    meta[line * nchunks + chunk] = m;
+  }
+}
+
+// cooperative copy of one coefficient image (KS * 4 KB) into shared memory
+template <int J, int NT>
+__device__ __forceinline__ void copy_coef_img(unsigned char* dst, const unsigned char* src, int tid) {
+  constexpr int n16 = tc_img_bytes<J>() / 16;
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int q = tid; q < n16; q += NT) d[q] = __ldg(s + q);
+}
+
+}  // namespace pgx

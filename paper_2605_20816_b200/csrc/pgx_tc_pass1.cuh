@@ -19,6 +19,7 @@
 #pragma once
 
 #include "pgx_grid_common.cuh"
+#include "pgx_tc_coeffs.cuh"
 #include "pgx_tc_common.cuh"
 
 namespace pgx {
@@ -75,7 +76,7 @@ struct TcP1Smem {
   static constexpr int KS = tc_ksteps(J);
   static constexpr int A_BYTES = R * KS * kTcThreads * 32;
   static constexpr int B_BYTES = KS * kTcChunk * 32;
-  static constexpr int BD_BYTES = kTcChunk * J * 8;
+  static constexpr int BD_BYTES = 0;  // exact B'' is read from the per-line table
   static constexpr int RARE_BYTES = R * kTcThreads * (int)sizeof(TcRare);
   static constexpr int A_OFF = 0;
   static constexpr int B_OFF = A_OFF + A_BYTES;
@@ -94,13 +95,11 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_tc_pass1(GridParams g) {
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* A_s = smem + L::A_OFF;
   unsigned char* B_s = smem + L::B_OFF;
-  double* Bd_s = reinterpret_cast<double*>(smem + L::BD_OFF);  // [256][J] exact B''
   TcRare* rare = reinterpret_cast<TcRare*>(smem + L::RARE_OFF);  // [R][128]
   __shared__ double lc[K];
   __shared__ uint64_t mbar;
   __shared__ unsigned tmem_base;
   __shared__ unsigned s_bmax;     // max over grains of sum_j |B''_j| (float bits)
-  __shared__ unsigned s_chmax;    // max |B''| of the current chunk (float bits)
   __shared__ double red_d[kTcThreads];
   __shared__ long long red_i[kTcThreads];
 
@@ -156,54 +155,21 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_tc_pass1(GridParams g) {
   const unsigned b_addr = (unsigned)__cvta_generic_to_shared(B_s);
   unsigned phase = 0;
 
-  // chunk [c0, c0 + cn): exact B'' -> Bd_s, scaled fp16 split -> B_s; returns 2^-sB
+  // chunk [c0, c0 + cn): copy the precomputed operand image (pgx_tc_coeffs.cuh)
+  // of this line into B_s; returns 2^-(sB + 10) so that D * this = h~''
+  const double* coef_line = g.tc_coef + line * (int64_t)N * J;  // exact B'' of this line
   auto build_chunk = [&](int c0, int cn) -> float {
+    (void)cn;
     __syncthreads();
-    if (tid == 0) s_chmax = 0u;
-    __syncthreads();
-    float bmax = 0.0f, b1max = 0.0f;
-    for (int q = tid; q < kTcChunk; q += kTcThreads) {
-      double B[J];
-      if (q < cn) {
-        line_coeffs<DIM, D>(g.theta, N, c0 + q, lc, c, B);
-      } else {
-#pragma unroll
-        for (int j = 0; j < J; ++j) B[j] = 0.0;
-      }
-      double bs = 0.0;
-#pragma unroll
-      for (int j = 0; j < J; ++j) {
-        Bd_s[q * J + j] = B[j];
-        bmax = fmaxf(bmax, (float)fabs(B[j]));
-        bs += fabs(B[j]);
-      }
-      b1max = fmaxf(b1max, (float)bs);
-    }
-    // non-finite or astronomically large coefficients poison the scale: the
-    // whole CTA then produces NaN (counted as non-finite, raised by the host)
-    atomicMax(&s_chmax, __float_as_uint(isfinite(bmax) ? bmax : CUDART_INF_F));
-    atomicMax(&s_bmax, __float_as_uint(isfinite(b1max) ? b1max : CUDART_INF_F));
-    __syncthreads();
-    const float chmax = __uint_as_float(s_chmax);
-    // scale 2^sB so that max |B''| 2^sB <= 2^14 (fp16 headroom)
-    const int sB = chmax > 0.0f ? 14 - ilogbf(chmax) - 1 : 0;
-    const double scl = ldexp(1.0, sB);
-    for (int q = tid; q < kTcChunk; q += kTcThreads) {
-      __half hi[J], lo[J];
-#pragma unroll
-      for (int j = 0; j < J; ++j) split_f16(Bd_s[q * J + j] * scl, hi[j], lo[j]);
-#pragma unroll
-      for (int k = 0; k < 16 * KS; ++k) {
-        const int b = k / J, j = k % J;
-        const __half val = k < 3 * J ? (b == 1 ? lo[j] : hi[j]) : __float2half(0.0f);
-        *reinterpret_cast<__half*>(B_s + (k / 16) * (kTcChunk * 32) + slab_off(q, k % 16)) = val;
-      }
-    }
+    const int64_t ci = line * g.tc_nchunks + c0 / kTcChunk;
+    copy_coef_img<J, kTcThreads>(B_s, g.tc_img + ci * tc_img_bytes<J>(), tid);
+    const int2 m = g.tc_meta[ci];
+    if (tid == 0) atomicMax(&s_bmax, (unsigned)m.y);  // non-negative float bits
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    return ldexpf(1.0f, -(sB + 10));  // D * this = h~''
+    return ldexpf(1.0f, -(m.x + 10));
   };
 
   // one UMMA tile: D[128 x 256] = A_r B^T, then wait for the accumulator
@@ -322,7 +288,8 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_tc_pass1(GridParams g) {
             while (cm) {
               const int q = __ffs(cm) - 1;
               cm &= cm - 1u;
-              tc_rare_update(st, c0 + cb + q, eval_line<J>(Bd_s + (cb + q) * J, u), c);
+              tc_rare_update(st, c0 + cb + q,
+                             eval_line<J>(coef_line + (int64_t)(c0 + cb + q) * J, u), c);
             }
           }
         }
@@ -343,9 +310,7 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_tc_pass1(GridParams g) {
     const int64_t p = pbase + kTcThreads * r + tid;
     double u[J];
     axis_table<D>(axis_coord(col, g.M), g.legendre != 0, u);
-    double Bg[J];
-    line_coeffs<DIM, D>(g.theta, N, lab[r], lc, c, Bg);
-    const double hG = eval_line<J>(Bg, u);
+    const double hG = eval_line<J>(coef_line + (int64_t)lab[r] * J, u);  // same bits as the refine
     TcRare& st = rare[r * kTcThreads + tid];
     const double refd = (double)ref[r];
     const double aG = hG - refd;

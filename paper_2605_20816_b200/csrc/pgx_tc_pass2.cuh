@@ -15,6 +15,7 @@
 #pragma once
 
 #include "pgx_grid_common.cuh"
+#include "pgx_tc_coeffs.cuh"
 #include "pgx_tc_common.cuh"
 
 namespace pgx {
@@ -92,43 +93,18 @@ __global__ void __launch_bounds__(kTc2Threads, 4) k_tc_pass2(GridParams g) {
   };
 
   for (int64_t line = l0; line < l1; ++line) {
-    // ---- per line: exact B'' of this thread's grain -> scaled fp16 split (A of UMMA 1)
+    // ---- per line: the precomputed operand image of this 128-grain tile (A of UMMA 1)
     __syncthreads();
     if (tid == 0) {
       double lcr[K];
       line_factors<DIM, D>(line, g, lcr);
 #pragma unroll
       for (int k = 0; k < K; ++k) lc[k] = lcr[k];
-      s_bmax = 0u;
     }
+    const int64_t ci = line * g.tc_nchunks + blockIdx.x;
+    copy_coef_img<J, kTc2Threads>(smem + L::A1_OFF, g.tc_img + ci * tc_img_bytes<J>(), tid);
+    const int sB = g.tc_meta[ci].x;
     __syncthreads();
-    double B[J];
-    if (active) {
-      line_coeffs<DIM, D>(g.theta, g.N, i, lc, g.c, B);
-    } else {
-#pragma unroll
-      for (int j = 0; j < J; ++j) B[j] = 0.0;
-    }
-    float bm = 0.0f;
-#pragma unroll
-    for (int j = 0; j < J; ++j) bm = fmaxf(bm, (float)fabs(B[j]));
-    atomicMax(&s_bmax, __float_as_uint(isfinite(bm) ? bm : CUDART_INF_F));
-    __syncthreads();
-    const float bmax = __uint_as_float(s_bmax);
-    const int sB = bmax > 0.0f ? 13 - ilogbf(bmax) : 0;
-    {
-      const double scl = ldexp(1.0, sB);
-      __half hi[J], lo[J];
-#pragma unroll
-      for (int j = 0; j < J; ++j) split_f16(B[j] * scl, hi[j], lo[j]);
-#pragma unroll
-      for (int k = 0; k < 16 * KS; ++k) {
-        const int b = k / J, j = k % J;
-        const __half val = k < 3 * J ? (b == 1 ? lo[j] : hi[j]) : __float2half(0.0f);
-        *reinterpret_cast<__half*>(smem + L::A1_OFF + (k / 16) * (kTc2Threads * 32) +
-                                   slab_off(tid, k % 16)) = val;
-      }
-    }
     const float inv = ldexpf(1.0f, -(sB + 10));  // S * inv = h~''
     double R64[J];
 #pragma unroll
