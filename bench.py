@@ -389,7 +389,9 @@ def run_ours(args):
             "cpu_baseline": cpu_baseline,
             "gpu_launches": launches,
             "clocks": clocks,
-            "result": {"phi": float(stats[0]), "err": float(stats[1]), "e0": float(stats[2])},
+            "result": {"phi": float(stats[0]), "err": float(stats[1]), "e0": float(stats[2]),
+                       "n_rescanned": int(stats[3]),
+                       "n_ambiguous": int(stats.view(np.int64)[6])},
         }
         print(json.dumps(line), flush=True)
     prob.close()

@@ -64,6 +64,7 @@ struct pgx_problem {
   int* d_fix_list = nullptr;
   int* d_counters = nullptr;      // [0] fix_count, [1] nonfinite grad
   long long* d_fix_correct = nullptr;
+  double* d_part_th2 = nullptr;   // tail: per-CTA lambda-norm partials
   double* d_part_d = nullptr;
   long long* d_part_i = nullptr;
   double* d_part_g = nullptr;
@@ -101,7 +102,7 @@ struct pgx_problem {
   }
   void release() {
     void* bufs[] = {d_points, d_labels, d_theta, d_theta_in, d_pix_m, d_pix_ls, d_fix_list,
-                    d_counters, d_fix_correct, d_part_d, d_part_i, d_part_g, d_grad, d_stats,
+                    d_counters, d_fix_correct, d_part_th2, d_part_d, d_part_i, d_part_g, d_grad, d_stats,
                     d_labels_out, d_margin_out, grid.d_part, grid.d_tc};
     for (void* b : bufs)
       if (b) cudaFree(b);
@@ -327,6 +328,7 @@ pgx_status pgx_problem_create(const pgx_desc* desc, pgx_problem** out) {
   A(pb->alloc(&pb->d_fix_list, (size_t)P));
   A(pb->alloc(&pb->d_counters, 4));
   A(pb->alloc(&pb->d_fix_correct, 2));
+  A(pb->alloc(&pb->d_part_th2, (size_t)4 * sms + 8));
   A(pb->alloc(&pb->d_part_d, (size_t)pb->blocks1 * 2));
   A(pb->alloc(&pb->d_part_i, (size_t)pb->blocks1 * 4));
   A(pb->alloc(&pb->d_part_g, (size_t)pb->splits * KN));
@@ -507,6 +509,7 @@ pgx_status pgx_eval(pgx_problem* pb, const void* theta, double eps, double lambd
   tp.want_grad = want_grad;
   tp.fix_amb = pb->grid.enabled ? 1 : 0;
   tp.ticket = reinterpret_cast<unsigned*>(pb->d_counters + 2);
+  tp.part_th2 = pb->d_part_th2;
   ReduceParams& rp = tp.red;
   rp.K = pb->K;
   rp.N = pb->N;
@@ -534,7 +537,7 @@ pgx_status pgx_eval(pgx_problem* pb, const void* theta, double eps, double lambd
   fp.stats_out = stats_dst;
   const int64_t KN = (int64_t)pb->K * pb->N;
   const int tail_blocks =
-      want_grad ? (int)std::min<int64_t>((KN + 31) / 32, 4 * pb->sms) : pb->sms;
+      want_grad ? (int)std::min<int64_t>((KN + 7) / 8, 4 * pb->sms) : pb->sms;
   pb->prof_begin("tail");
   PGX_DISPATCH(launch_tail, prm, tp, tail_blocks, s);
   pb->prof_end();
@@ -577,6 +580,7 @@ pgx_status pgx_assign(pgx_problem* pb, const void* theta, uint32_t flags, int64_
   TailParams tp{};
   tp.want_grad = 0;
   tp.ticket = reinterpret_cast<unsigned*>(pb->d_counters + 2);
+  tp.part_th2 = pb->d_part_th2;
   FinalParams& fp = tp.fin;
   fp.blocks1 = pb->blocks1;
   fp.K = pb->K;

@@ -407,6 +407,7 @@ struct TailParams {
   int want_grad;
   int fix_amb;  // the re-scan decides the ambiguity of queued points (grid path)
   unsigned* ticket;
+  double* part_th2;  // [gridDim.x] per-CTA partials of ||theta[:, :N-1]||^2
 };
 
 constexpr int kTailThreads = 256;
@@ -471,28 +472,47 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(EvalParams e, TailParams 
     }
   }
 
-  // (2) gradient: CTA b owns entries [32 b, 32 b + 32)
-  if (t.want_grad) {
+  // (2) gradient: warp w of CTA b owns entries ent = 8 b + w (grid-strided);
+  // it also accumulates its entries' share of ||theta[:, :N-1]||^2 for the
+  // lambda term (fixed order)
+  double th2 = 0.0;
+  {
     const ReduceParams& r = t.red;
-    const int64_t KN = (int64_t)r.K * r.N;
-    for (int64_t base = (int64_t)blockIdx.x * 32; base < KN; base += (int64_t)gridDim.x * 32) {
-      const int64_t ent = base + lane;
-      double a = 0.0;
-      if (ent < KN)
-        for (int s = warp; s < r.splits; s += 8) a += r.part_g[s * KN + ent];
-      sred[warp][lane] = a;
-      __syncthreads();
-      if (warp == 0 && ent < KN) {
-        double acc = 0.0;
+    const int64_t KN = (int64_t)t.fin.K * t.fin.N;
+    const bool lam = t.fin.lambda != 0.0;
+    if (t.want_grad || lam) {
+      // one warp per entry, lanes over the splits (s = lane mod 32), fixed
+      // shuffle tree: many loads in flight, deterministic order
+      const int nw = gridDim.x * (kTailThreads / 32);
+      for (int64_t ent = (int64_t)blockIdx.x * (kTailThreads / 32) + warp; ent < KN; ent += nw) {
+        double a = 0.0;
+        if (t.want_grad) {
+#pragma unroll 4
+          for (int s = lane; s < r.splits; s += 32) a += r.part_g[s * KN + ent];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) acc += sred[w][lane];
-        double gv = -acc / (r.eps * (double)r.P);  // objective.py:162
-        const int i = (int)(ent % r.N);
-        if (r.lambda != 0.0 && i < r.N - 1) gv -= r.lambda * r.theta[ent];
-        if (!isfinite(gv)) atomicAdd(r.nonfinite, 1);
-        r.grad_out[ent] = gv;
+          for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+        }
+        if (lane == 0) {
+          const int i = (int)(ent % t.fin.N);
+          const double th = t.fin.theta[ent];
+          if (lam && i < t.fin.N - 1) th2 += th * th;
+          if (t.want_grad) {
+            double gv = -a / (r.eps * (double)r.P);  // objective.py:162
+            if (lam && i < r.N - 1) gv -= r.lambda * th;
+            if (!isfinite(gv)) atomicAdd(r.nonfinite, 1);
+            r.grad_out[ent] = gv;
+          }
+        }
       }
-      __syncthreads();
+    }
+    // per-CTA partial of the lambda norm: lane 0 of each warp, fixed order
+    if (lane == 0) sred[warp][0] = th2;
+    __syncthreads();
+    if (tid == 0) {
+      double s8 = 0.0;
+#pragma unroll
+      for (int w = 0; w < kTailThreads / 32; ++w) s8 += sred[w][0];
+      t.part_th2[blockIdx.x] = s8;
     }
   }
 
@@ -510,6 +530,7 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(EvalParams e, TailParams 
   const int b0 = tid * per, b1 = min(prm.blocks1, b0 + per);
   double ell = 0.0, e0 = 0.0;
   long long cor = 0, amb = 0, nf = 0;
+#pragma unroll 4
   for (int b = b0; b < b1; ++b) {
     ell += prm.part_d[2 * b + 0];
     e0 += prm.part_d[2 * b + 1];
@@ -517,12 +538,10 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(EvalParams e, TailParams 
     amb += prm.part_i[4 * b + 1];
     nf += prm.part_i[4 * b + 2];
   }
-  double th2 = 0.0;
-  if (prm.lambda != 0.0) {
-    const int64_t KN = (int64_t)prm.K * prm.N;
-    const int64_t per2 = (KN + kTailThreads - 1) / kTailThreads;
-    for (int64_t q = tid * per2; q < min(KN, (tid + 1) * per2); ++q)
-      if (q % prm.N < prm.N - 1) th2 += prm.theta[q] * prm.theta[q];
+  th2 = 0.0;
+  if (prm.lambda != 0.0) {  // per-CTA partials of phase (2), fixed order
+    const int per2 = (gridDim.x + kTailThreads - 1) / kTailThreads;
+    for (int q = tid * per2; q < min((int)gridDim.x, (tid + 1) * per2); ++q) th2 += t.part_th2[q];
   }
   ell = block_sum<kTailThreads>(ell, rd);
   e0 = block_sum<kTailThreads>(e0, rd);
