@@ -103,7 +103,7 @@ struct pgx_problem {
   void release() {
     void* bufs[] = {d_points, d_labels, d_theta, d_theta_in, d_pix_m, d_pix_ls, d_fix_list,
                     d_counters, d_fix_correct, d_part_th2, d_part_d, d_part_i, d_part_g, d_grad, d_stats,
-                    d_labels_out, d_margin_out, grid.d_part, grid.d_tc};
+                    d_labels_out, d_margin_out, grid.d_part, grid.d_tc, grid.d_tc_pix};
     for (void* b : bufs)
       if (b) cudaFree(b);
     for (cudaEvent_t& e : prof_ev)

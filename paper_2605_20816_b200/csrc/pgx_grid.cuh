@@ -26,10 +26,15 @@ struct GridPlan {
   double* tc_coef = nullptr;
   unsigned char* tc_img = nullptr;
   int2* tc_meta = nullptr;
+  void* d_tc_pix = nullptr;                        // pass-2 pixel operand tiles (once per problem)
+  unsigned char* tc_pix = nullptr;
+  bool tc_pix_ready = false;
+  float* tc_rec = nullptr;                         // pass-2 pixel records (aliases pix_w | pix_q)
+  double* tc_lc = nullptr;                         // [lines][K] line factors
   int GT = 128, gtiles = 1, splits = 1, lines_per_split = 1;
   int splits_out = 1;
   double* part_out = nullptr;
-  void* d_part = nullptr;  // single allocation: part_g | pix_w | pix_q
+  void* d_part = nullptr;  // single allocation: part_g | pix_w, pix_q (fp64) or tc_rec (TC)
   double* pix_w = nullptr;
   float* pix_q = nullptr;
   int smem2 = 0;
@@ -80,11 +85,24 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
   const int K = feature_count(d->dim, d->degree);
   gp.smem2 = K * kG2Threads * 8;
   if (gp.tc && side % kTc2Px == 0) {
-    // tensor-core pass 2: 128-grain tiles x line ranges, 4 CTAs per SM
-    gp.tc2_gtiles = (N + kTc2Threads - 1) / kTc2Threads;
-    int sp = std::max(1, std::min(gp.lines, (8 * sms + gp.tc2_gtiles - 1) / gp.tc2_gtiles));
-    gp.tc2_lps = (gp.lines + sp - 1) / sp;
-    gp.tc2_splits = (gp.lines + gp.tc2_lps - 1) / gp.tc2_lps;
+    // tensor-core pass 2: 128-grain tiles x line ranges, 2 CTAs per SM; the
+    // split count minimises waves x lines-per-CTA (ties: fewer splits, so the
+    // tail reduces less)
+    gp.tc2_gtiles = (N + kTc2Grains - 1) / kTc2Grains;
+    const int64_t slots = 2LL * sms;
+    int64_t best = -1;
+    for (int sp = 1; sp <= std::min(gp.lines, 8 * sms); ++sp) {
+      const int lps = (gp.lines + sp - 1) / sp;
+      const int spr = (gp.lines + lps - 1) / lps;
+      if (spr != sp) continue;
+      const int64_t waves = ((int64_t)gp.tc2_gtiles * spr + slots - 1) / slots;
+      const int64_t cost = waves * (lps + 1);  // + ~1 line of per-CTA pipeline fill
+      if (best < 0 || cost < best) {
+        best = cost;
+        gp.tc2_lps = lps;
+        gp.tc2_splits = spr;
+      }
+    }
     gp.splits_out = gp.tc2_splits;
     gp.part_splits = std::max(gp.splits, gp.tc2_splits);
   }
@@ -95,7 +113,7 @@ inline size_t grid_workspace_bytes(const pgx_desc* d, int sms) {
   grid_plan_shape(gp, d, sms);
   if (!gp.enabled) return 0;
   const int K = feature_count(d->dim, d->degree);
-  return (size_t)std::max(gp.splits, gp.part_splits) * K * d->n_grains * 8 + (size_t)d->n_points * 12;
+  return (size_t)std::max(gp.splits, gp.part_splits) * K * d->n_grains * 8 + (size_t)d->n_points * 16;
 }
 
 inline cudaError_t grid_plan_create(GridPlan& gp, const pgx_desc* d, int sms, size_t& bytes) {
@@ -103,7 +121,7 @@ inline cudaError_t grid_plan_create(GridPlan& gp, const pgx_desc* d, int sms, si
   if (!gp.enabled) return cudaSuccess;
   const int K = feature_count(d->dim, d->degree);
   const size_t part = (size_t)std::max(gp.splits, gp.part_splits) * K * d->n_grains;
-  const size_t n = part * 8 + (size_t)d->n_points * 8 + (size_t)d->n_points * 4 + 256;
+  const size_t n = part * 8 + (size_t)d->n_points * 16 + 256;
   cudaError_t e = cudaMalloc(&gp.d_part, n);
   if (e != cudaSuccess) return e;
   bytes += n;
@@ -116,13 +134,25 @@ inline cudaError_t grid_plan_create(GridPlan& gp, const pgx_desc* d, int sms, si
     const size_t ncoef = (size_t)gp.lines * d->n_grains * J;
     const size_t nimg = (size_t)gp.lines * gp.tc_nchunks * tc_ksteps(J) * kTcCoefChunk * 32;
     const size_t nmeta = (size_t)gp.lines * gp.tc_nchunks;
-    const size_t tb = ncoef * 8 + nimg + nmeta * 8 + 256;
+    const size_t nlc = (size_t)gp.lines * K;
+    const size_t tb = ncoef * 8 + nimg + nmeta * 8 + nlc * 8 + 256;
     e = cudaMalloc(&gp.d_tc, tb);
     if (e != cudaSuccess) return e;
     bytes += tb;
     gp.tc_coef = static_cast<double*>(gp.d_tc);
     gp.tc_img = reinterpret_cast<unsigned char*>(gp.tc_coef + ncoef);
     gp.tc_meta = reinterpret_cast<int2*>(gp.tc_img + nimg);
+    gp.tc_lc = reinterpret_cast<double*>(gp.tc_meta + nmeta);
+    if (gp.tc2_splits > 0) {
+      gp.tc_rec = reinterpret_cast<float*>(gp.pix_w);  // 16 bytes per pixel
+      const size_t npix = (size_t)(2 * d->resolution / kTcPixTile) *
+                          (tc_ksteps(J) * kTcPixTile * 32 + 2 * (kTcPixTile / 16) * 16 * 32);
+      e = cudaMalloc(&gp.d_tc_pix, npix);
+      if (e != cudaSuccess) return e;
+      bytes += npix;
+      gp.tc_pix = static_cast<unsigned char*>(gp.d_tc_pix);
+      gp.tc_pix_ready = false;
+    }
   }
   return cudaSuccess;
 }
@@ -169,9 +199,15 @@ inline void tc_dispatch_coeffs(const GridParams& g, const GridPlan& gp, cudaStre
 }
 
 template <int DIM, int D>
+inline void tc_dispatch_pix(const GridParams& g, const GridPlan& gp, cudaStream_t s) {
+  k_tc_pix<D><<<g.side / kTcPixTile, kTcPixTile, 0, s>>>(g.M, g.legendre, gp.tc_pix);
+}
+
+template <int DIM, int D>
 inline void tc_dispatch_pass2(const GridParams& g, dim3 grid, cudaStream_t s) {
   auto kern = k_tc_pass2<DIM, D>;
-  const int smem = std::max(TcP2Smem<D + 1>::TOTAL, kTcMinSmem);
+  // padded so that <= 2 CTAs (2 x 256 TMEM columns) share an SM
+  const int smem = std::max(TcP2Smem<D + 1>::TOTAL, 80 * 1024);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -260,6 +296,19 @@ inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool wa
   g.tc_img = gp.tc_img;
   g.tc_meta = gp.tc_meta;
   g.tc_nchunks = gp.tc_nchunks;
+  g.tc_pix = gp.tc_pix;
+  g.tc_lc = gp.tc_lc;
+  g.tc_rec = want_grad ? gp.tc_rec : nullptr;
+  if (gp.tc && gp.tc_pix && !gp.tc_pix_ready) {  // once per problem
+    if (gp.dim == 2) {
+      PGX_GRID_DEG(2, tc_dispatch_pix, g, gp, s)
+    } else {
+      PGX_GRID_DEG3(tc_dispatch_pix, g, gp, s)
+    }
+    ++*launches;
+    if (cudaPeekAtLastError() != cudaSuccess) return PGX_ERR_CUDA;
+    gp.tc_pix_ready = true;
+  }
   if (gp.tc) {
     prof.begin(prof.ctx, "tc_coeffs");
     if (gp.dim == 2) {

@@ -105,6 +105,10 @@ struct GridParams {
   const unsigned char* tc_img;  // [lines][chunks] UMMA operand images
   const int2* tc_meta;          // [lines][chunks] {sB, bnorm bits}
   int tc_nchunks;
+  double* tc_lc;                // [lines][K] line factors (k_tc_coeffs)
+  const unsigned char* tc_pix;  // [side / 64] pass-2 pixel operand tiles (k_tc_pix)
+  float* tc_rec;                // [lines][side / 64][4][64] pass-2 pixel records
+                                // (w13, wl13, qn, label) written by TC pass 1
 };
 
 // Per-line factors: lc[k] = prod over the non-fast axes of u_axis[alpha]

@@ -49,6 +49,10 @@ __global__ void __launch_bounds__(kTcCoefChunk) k_tc_coeffs(GridParams g, double
     line_factors<DIM, D>(line, g, lcr);
 #pragma unroll
     for (int k = 0; k < K; ++k) lc[k] = lcr[k];
+    if (chunk == 0 && g.tc_lc) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) g.tc_lc[line * K + k] = lcr[k];
+    }
     s_max = 0u;
     s_b1 = 0u;
   }
@@ -99,6 +103,56 @@ __global__ void __launch_bounds__(kTcCoefChunk) k_tc_coeffs(GridParams g, double
     m.sB = sB;
     m.bnorm = __uint_as_float(s_b1);
     meta[line * nchunks + chunk] = m;
+  }
+}
+
+// ------------------------------------------------------------------ pixel tables
+// Pass-2 pixel operands of one 64-pixel tile of the fast axis (they depend on
+// the column only, so one table serves every line; built once per problem):
+//   [0, KS*2048)          UMMA 1 B: 64 rows (pixels) x K, pattern [hi, hi, lo]
+//                         of the 2^10-scaled fp16 split of u_j(x)
+//   [KS*2048, +2048)      UMMA 2 B, hi: 16 rows (j, zero-padded) x K = 64 pixels
+//   [KS*2048+2048, +2048) UMMA 2 B, lo
+constexpr int kTcPixTile = 64;
+
+template <int J>
+__host__ __device__ constexpr int tc_pix_bytes() {
+  return tc_ksteps(J) * kTcPixTile * 32 + 2 * (kTcPixTile / 16) * 16 * 32;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kTcPixTile) k_tc_pix(int M, int legendre,
+                                                       unsigned char* __restrict__ pix) {
+  constexpr int J = D + 1;
+  constexpr int KS = tc_ksteps(J);
+  const int tid = threadIdx.x;
+  const int col = blockIdx.x * kTcPixTile + tid;
+  unsigned char* dst = pix + (int64_t)blockIdx.x * tc_pix_bytes<J>();
+  double u[J];
+  axis_table<D>(axis_coord(col, M), legendre != 0, u);
+  __half hi[J], lo[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) split_f16(u[j] * 1024.0, hi[j], lo[j]);
+#pragma unroll
+  for (int s = 0; s < KS; ++s) {
+    __half row[16];
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      const int k = s * 16 + kk;
+      const int b = k / J, j = k % J;
+      row[kk] = k < 3 * J ? (b < 2 ? hi[j] : lo[j]) : __float2half(0.0f);
+    }
+    unsigned char* slab = dst + s * (kTcPixTile * 32);
+    *reinterpret_cast<uint4*>(slab + slab_off(tid, 0)) = *reinterpret_cast<const uint4*>(row);
+    *reinterpret_cast<uint4*>(slab + slab_off(tid, 8)) = *reinterpret_cast<const uint4*>(row + 8);
+  }
+  unsigned char* lh = dst + KS * (kTcPixTile * 32);
+  unsigned char* ll = lh + (kTcPixTile / 16) * 16 * 32;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const unsigned off = (tid / 16) * (16 * 32) + slab_off(j, tid % 16);
+    *reinterpret_cast<__half*>(lh + off) = j < J ? hi[j] : __float2half(0.0f);
+    *reinterpret_cast<__half*>(ll + off) = j < J ? lo[j] : __float2half(0.0f);
   }
 }
 

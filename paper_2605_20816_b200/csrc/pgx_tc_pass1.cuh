@@ -320,8 +320,15 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_tc_pass1(GridParams g) {
     const double l = (-aG - l2s) * 0.69314718055994530942;  // log p_G: objective.py:103-106
     ell += l;
     if (!isfinite(l) || !(bnorm <= 3e38f)) nonfinite = 1;
-    g.pix_w[p] = refd - 1.0 - l2s;
-    g.pix_q[p] = (float)(0.5 * sx64[r] / s);
+    if (g.tc_rec) {  // pass-2 record: p_i/2 * 2^13 = 2^(w13 + wl13 - h~''_i)
+      const double w13 = refd - 1.0 - l2s + 13.0;
+      const float wh = (float)w13;
+      float* rec = g.tc_rec + (line * (g.side / kTcPixTile) + (col >> 6)) * (4 * kTcPixTile) + (col & 63);
+      rec[0] = wh;
+      rec[kTcPixTile] = (float)(w13 - (double)wh);
+      rec[2 * kTcPixTile] = (float)(-4096.0 * sx64[r] / s);  // -(1 - p_G)/2 * 2^13
+      reinterpret_cast<int*>(rec)[3 * kTcPixTile] = lab[r];
+    }
     const bool found = st.cnt > 0 && !(st.flags & 2);
     const double m = st.cnt > 0 ? st.m : hG;
     g.pix_m[p] = m / c;

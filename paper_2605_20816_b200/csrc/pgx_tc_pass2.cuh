@@ -2,16 +2,29 @@
 // sum_x (onehot_G(x) - p(x)) eta(x) (objective.py:109-113) with BOTH
 // contractions on the tensor cores (FlashAttention-backward-like, grain-major):
 //
-//   UMMA 1  S^T[128 grains x 64 px] = B''(line)[grains x 3J] . L(x)[px x 3J]^T
-//   epilogue (thread = grain = TMEM lane): p/2 = 2^(w_x - h~''), r/2 = label ?
-//           q_x : -p/2, split into fp16 hi/lo, stored as the K-major A operand
-//   UMMA 2  R[128 grains x 16] += [r_hi r_hi r_lo] . [L_hi L_lo L_hi]^T
-//           (K = 3 x 64 pixels, fp32 accumulate in TMEM)
+//   UMMA 1 (SS)  S^T[128 grains x 64 px] = B''(line)[grains x 3J] . L(x)[px x 3J]^T
+//   epilogue     thread = grain = TMEM lane: r' = p/2 * 2^13 = 2^(w13 - h~''),
+//                or -(1 - p_G)/2 * 2^13 on the pixel's label grain; split into
+//                fp16 hi/lo and written BACK into TMEM over S (packed pairs)
+//   UMMA 2 (TS)  R[128 grains x 16] += [r'_hi r'_hi r'_lo]_tmem . [L_hi L_lo L_hi]^T
+//                (A operand from TMEM, K = 3 x 64 pixels, fp32 accumulate)
 //
-// R is flushed every 4 tiles into fp64 line sums and expanded per line into
-// the K gradient rows (fp64 shared memory), as in the CUDA-core grid pass 2.
-// CTA: 128 threads, one 128-grain tile, a range of lines; TMEM: 64 + 16
-// columns (alloc 128) so 4 CTAs share an SM.
+// Warp specialisation (FlashAttention-4 style), 288 threads, 2 CTAs per SM:
+//   warps 0-7  epilogue: warp w owns TMEM lanes 32 (w % 4) .. (grains) and the
+//              pixel half w / 4 of each tile (32 pixels);
+//   warp 8     producer: bulk async copies (cp.async.bulk + mbarrier tx counts)
+//              of the per-line coefficient image, the tile's pixel operands (one
+//              table per problem) and the tile's pass-1 records; issues UMMA 2 of
+//              tile n and UMMA 1 of tile n + 3 as soon as the epilogue of tile n
+//              has written r' — S is triple-buffered in TMEM, so the tensor core
+//              computes logits well ahead of the epilogue's exponentials.
+// R alternates between two TMEM accumulators per group of 4 tiles; a finished
+// group is flushed into fp64 line sums three tiles later (when it is known to
+// be complete) and per line expanded into the K gradient rows.
+//
+// TMEM (256 columns): S_0..S_2 [0, 192) (64 each), R_a [192, 208), R_b [208, 224).
+// Within S_s, pixel half h keeps r'_hi in [32h, 32h + 16) and r'_lo in
+// [32h + 16, 32h + 32): only columns its own warps have already read.
 #pragma once
 
 #include "pgx_grid_common.cuh"
@@ -20,29 +33,65 @@
 
 namespace pgx {
 
-constexpr int kTc2Threads = 128;
-constexpr int kTc2Px = 64;        // pixels per tile (UMMA 1 N, UMMA 2 K per product)
-constexpr int kTc2Flush = 4;      // tiles per fp32 -> fp64 flush of R
-constexpr float kTc2RScale = 8192.0f;  // r/2 scaled by 2^13 into the fp16 range
+constexpr int kTc2Epi = 256;              // epilogue threads (8 warps)
+constexpr int kTc2Threads = kTc2Epi + 32;  // + producer warp
+constexpr int kTc2Grains = 128;           // grains per CTA (TMEM lanes)
+constexpr int kTc2Px = kTcPixTile;        // pixels per tile
+constexpr int kTc2Group = 4;              // tiles per fp32 R group before the fp64 flush
+constexpr int kTc2S = 3;                  // S stages in TMEM (UMMA 1 runs 3 tiles ahead)
+constexpr int kTc2Buf = 6;                // tile buffers (pixel operands + records)
+constexpr int kTc2RecFloats = 4 * kTc2Px;  // w13[64] | wl13[64] | qn[64] | label[64]
 
 template <int J>
 struct TcP2Smem {
   static constexpr int KS = tc_ksteps(J);
-  static constexpr int A1 = KS * kTc2Threads * 32;   // B'' operand (128 rows)
-  static constexpr int B1 = KS * kTc2Px * 32;        // L operand (64 rows)
-  static constexpr int RPART = (kTc2Px / 16) * kTc2Threads * 32;  // r_hi or r_lo (16 KB)
-  static constexpr int LPART = (kTc2Px / 16) * 16 * 32;           // L_hi or L_lo (2 KB)
+  static constexpr int A1 = KS * kTc2Grains * 32;  // coefficient image (128 rows)
+  static constexpr int PIX = tc_pix_bytes<J>();
+  static constexpr int REC = kTc2RecFloats * 4;
   static constexpr int A1_OFF = 0;
-  static constexpr int B1_OFF = A1_OFF + A1;
-  static constexpr int RH_OFF = B1_OFF + B1;
-  static constexpr int RL_OFF = RH_OFF + RPART;
-  static constexpr int LH_OFF = RL_OFF + RPART;
-  static constexpr int LL_OFF = LH_OFF + LPART;
-  static constexpr int TOTAL = LL_OFF + LPART;
+  static constexpr int PIX_OFF = A1_OFF + 2 * A1;
+  static constexpr int REC_OFF = PIX_OFF + kTc2Buf * PIX;
+  static constexpr int TOTAL = REC_OFF + kTc2Buf * REC;
+};
+
+// registers written by an async TMEM load become usable after the wait; the
+// empty asm ties every use to it
+template <int N>
+__device__ __forceinline__ void tmem_regs_ready(uint32_t (&r)[N]) {
+#pragma unroll
+  for (int q = 0; q < N; ++q) asm volatile("" : "+r"(r[q]));
+}
+__device__ __forceinline__ void tmem_ld32_nowait(unsigned taddr, uint32_t (&s0)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(s0[0]), "=r"(s0[1]), "=r"(s0[2]), "=r"(s0[3]), "=r"(s0[4]), "=r"(s0[5]), "=r"(s0[6]),
+        "=r"(s0[7]), "=r"(s0[8]), "=r"(s0[9]), "=r"(s0[10]), "=r"(s0[11]), "=r"(s0[12]),
+        "=r"(s0[13]), "=r"(s0[14]), "=r"(s0[15]), "=r"(s0[16]), "=r"(s0[17]), "=r"(s0[18]),
+        "=r"(s0[19]), "=r"(s0[20]), "=r"(s0[21]), "=r"(s0[22]), "=r"(s0[23]), "=r"(s0[24]),
+        "=r"(s0[25]), "=r"(s0[26]), "=r"(s0[27]), "=r"(s0[28]), "=r"(s0[29]), "=r"(s0[30]),
+        "=r"(s0[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+
+// (line index, tile) walk over a CTA's items without divisions
+struct Tc2Cursor {
+  int n = 0, li = 0, t = 0;
+  __device__ __forceinline__ void advance(int ntiles) {
+    ++n;
+    if (++t == ntiles) {
+      t = 0;
+      ++li;
+    }
+  }
 };
 
 template <int DIM, int D>
-__global__ void __launch_bounds__(kTc2Threads, 4) k_tc_pass2(GridParams g) {
+__global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
   constexpr int J = D + 1;
   constexpr int K = feature_count(DIM, D);
   using L = TcP2Smem<J>;
@@ -50,188 +99,224 @@ __global__ void __launch_bounds__(kTc2Threads, 4) k_tc_pass2(GridParams g) {
   constexpr uint32_t IDESC1 = umma_idesc_f16(128, kTc2Px);
   constexpr uint32_t IDESC2 = umma_idesc_f16(128, 16);
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ double lc[K];
-  __shared__ __align__(16) float w_s[kTc2Px], wl_s[kTc2Px], q_s[kTc2Px];
-  __shared__ __align__(16) int lab_s[kTc2Px];
-  __shared__ uint64_t mbar;
+  __shared__ uint64_t bar_full[kTc2Buf], bar_a[2], bar_s[kTc2S], bar_p[kTc2S], bar_end;
   __shared__ unsigned tmem_base;
-  __shared__ unsigned s_bmax;
 
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int i = blockIdx.x * kTc2Threads + tid;  // this thread's grain (TMEM lane)
-  const bool active = i < g.N;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gbase = blockIdx.x * kTc2Grains;
   const int64_t l0 = (int64_t)blockIdx.y * g.lines_per_split;
-  const int64_t l1 = min((int64_t)g.lines, l0 + g.lines_per_split);
+  const int nlines = (int)(min((int64_t)g.lines, l0 + g.lines_per_split) - l0);
+  const int ntiles = g.side / kTc2Px;
+  const int gpl = (ntiles + kTc2Group - 1) / kTc2Group;  // R groups per line
+  const int nitems = nlines * ntiles;
+  if (nitems <= 0) return;
 
-  if (warp == 0) tmem_alloc(&tmem_base, 128);
-  if (tid == 0) {
-    mbar_init(&mbar, 1);
+  if (warp == 8) tmem_alloc(&tmem_base, 256);
+  if (tid == kTc2Epi) {
+    for (int b = 0; b < kTc2Buf; ++b) mbar_init(&bar_full[b], 1);
+    for (int b = 0; b < kTc2S; ++b) {
+      mbar_init(&bar_s[b], 1);
+      mbar_init(&bar_p[b], kTc2Epi / 32);
+    }
+    mbar_init(&bar_a[0], 1);
+    mbar_init(&bar_a[1], 1);
+    mbar_init(&bar_end, 1);
     fence_mbar_init();
   }
-  // fp64 gradient rows of this thread's grain accumulate in place in part_g
-  double* acc = g.part_g + (int64_t)blockIdx.y * K * g.N + (active ? i : 0);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const unsigned tmem = tmem_base;
-  const unsigned t_s = tmem;        // S^T: columns [0, 64)
-  const unsigned t_r = tmem + 64;   // R:   columns [64, 80)
-  const unsigned lane_off = (unsigned)(warp * 32) << 16;
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
-  unsigned phase = 0;
-
-  auto sync_tc = [&]() {
-    fence_proxy_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
+  auto group_last = [&](const Tc2Cursor& c) {
+    return c.t == ntiles - 1 || c.t % kTc2Group == kTc2Group - 1;
   };
-  auto wait_mma = [&]() {
-    mbar_wait(&mbar, phase);
-    phase ^= 1u;
-    tc_fence_after();
+  auto r_col = [&](const Tc2Cursor& c) {  // R accumulator of the item's group
+    return tmem + 192u + 16u * (unsigned)((c.li * gpl + c.t / kTc2Group) & 1);
   };
 
-  for (int64_t line = l0; line < l1; ++line) {
-    // ---- per line: the precomputed operand image of this 128-grain tile (A of UMMA 1)
-    __syncthreads();
-    if (tid == 0) {
-      double lcr[K];
-      line_factors<DIM, D>(line, g, lcr);
-#pragma unroll
-      for (int k = 0; k < K; ++k) lc[k] = lcr[k];
-    }
-    const int64_t ci = line * g.tc_nchunks + blockIdx.x;
-    copy_coef_img<J, kTc2Threads>(smem + L::A1_OFF, g.tc_img + ci * tc_img_bytes<J>(), tid);
-    const int sB = g.tc_meta[ci].x;
-    __syncthreads();
-    const float inv = ldexpf(1.0f, -(sB + 10));  // S * inv = h~''
-    double R64[J];
-#pragma unroll
-    for (int j = 0; j < J; ++j) R64[j] = 0.0;
-    const int64_t pline = line * g.side;
-    const int ntiles = g.side / kTc2Px;
-
-    for (int t = 0; t < ntiles; ++t) {
-      // ---- per tile: pixel operands (UMMA 1 B, UMMA 2 B) and per-pixel records
-      if (tid < kTc2Px) {
-        const int col = t * kTc2Px + tid;
-        double u[J];
-        axis_table<D>(axis_coord(col, g.M), g.legendre != 0, u);
-        __half hi[J], lo[J];
-#pragma unroll
-        for (int j = 0; j < J; ++j) split_f16(u[j] * 1024.0, hi[j], lo[j]);
-#pragma unroll
-        for (int k = 0; k < 16 * KS; ++k) {
-          const int b = k / J, j = k % J;
-          const __half val = k < 3 * J ? (b < 2 ? hi[j] : lo[j]) : __float2half(0.0f);
-          *reinterpret_cast<__half*>(smem + L::B1_OFF + (k / 16) * (kTc2Px * 32) +
-                                     slab_off(tid, k % 16)) = val;
-        }
-        // UMMA 2 B operand: rows j (N = 16), K = pixels
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const __half h = j < J ? hi[j] : __float2half(0.0f);
-          const __half l = j < J ? lo[j] : __float2half(0.0f);
-          const unsigned off = (tid / 16) * (16 * 32) + slab_off(j, tid % 16);
-          *reinterpret_cast<__half*>(smem + L::LH_OFF + off) = h;
-          *reinterpret_cast<__half*>(smem + L::LL_OFF + off) = l;
-        }
-        const double wd = g.pix_w[pline + col];
-        w_s[tid] = (float)wd;
-        wl_s[tid] = (float)(wd - (double)(float)wd);
-        q_s[tid] = g.pix_q[pline + col] * kTc2RScale;
-        lab_s[tid] = g.labels[pline + col];
+  if (warp == 8) {
+    // ======================= producer / MMA warp: the loop is warp-uniform,
+    // one lane issues the copies and the MMAs
+    const bool leader = lane == 0;
+    const uint64_t d_a1 = umma_desc(sbase + L::A1_OFF);
+    const uint64_t d_pix = umma_desc(sbase + L::PIX_OFF);
+    Tc2Cursor cl, cs, cm, cw;  // next load, next UMMA 1, next UMMA 2, next completion check
+    auto load_next = [&]() {
+      const int b = cl.n % kTc2Buf;
+      if (leader) {
+        mbar_arrive_expect_tx(&bar_full[b], L::PIX + L::REC);
+        bulk_g2s(smem + L::PIX_OFF + b * L::PIX, g.tc_pix + (int64_t)cl.t * L::PIX, L::PIX,
+                 &bar_full[b]);
+        bulk_g2s(smem + L::REC_OFF + b * L::REC,
+                 g.tc_rec + ((l0 + cl.li) * ntiles + cl.t) * (int64_t)kTc2RecFloats, L::REC,
+                 &bar_full[b]);
       }
-      sync_tc();
-      if (tid == 0) {
+      cl.advance(ntiles);
+    };
+    auto load_coef = [&](int li) {
+      const int b = li & 1;
+      if (leader) {
+        mbar_arrive_expect_tx(&bar_a[b], L::A1);
+        bulk_g2s(smem + L::A1_OFF + b * L::A1,
+                 g.tc_img + ((l0 + li) * g.tc_nchunks + blockIdx.x) * (int64_t)L::A1, L::A1,
+                 &bar_a[b]);
+      }
+    };
+    auto issue_s = [&]() {  // UMMA 1 of item cs into S_(n % 3)
+      const int b = cs.n % kTc2Buf, st = cs.n % kTc2S;
+      if (cs.t == 0) mbar_wait(&bar_a[cs.li & 1], (unsigned)(cs.li >> 1) & 1u);
+      mbar_wait(&bar_full[b], (unsigned)(cs.n / kTc2Buf) & 1u);
+      tc_fence_after();
+      if (leader) {
+        const uint64_t da = d_a1 + (uint64_t)(((cs.li & 1) * L::A1) >> 4);
+        const uint64_t db = d_pix + (uint64_t)((b * L::PIX) >> 4);
 #pragma unroll
         for (int s = 0; s < KS; ++s)
-          umma_f16_ss(t_s, umma_desc(sbase + L::A1_OFF + s * (kTc2Threads * 32)),
-                      umma_desc(sbase + L::B1_OFF + s * (kTc2Px * 32)), IDESC1, s > 0);
-        umma_commit(&mbar);
+          umma_f16_ss(tmem + 64u * st, da + (uint64_t)((s * kTc2Grains * 32) >> 4),
+                      db + (uint64_t)((s * kTc2Px * 32) >> 4), IDESC1, s > 0);
+        umma_commit(&bar_s[st]);
       }
-      wait_mma();
-
-      // ---- epilogue: r/2 * 2^13 as fp16 hi/lo into the UMMA 2 A operand
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        float v[32];
-        tmem_ld32(t_s + lane_off + half * 32, v);
-#pragma unroll
-        for (int q8 = 0; q8 < 32; q8 += 8) {
-          uint32_t ph[4], pl[4];
-          float wv[8], wlv[8], qv[8];
-          int lv[8];
-          {  // per-pixel records of these 8 pixels: 128-bit broadcast loads
-            const int x0 = half * 32 + q8;
-            *reinterpret_cast<float4*>(wv) = *reinterpret_cast<const float4*>(w_s + x0);
-            *reinterpret_cast<float4*>(wv + 4) = *reinterpret_cast<const float4*>(w_s + x0 + 4);
-            *reinterpret_cast<float4*>(wlv) = *reinterpret_cast<const float4*>(wl_s + x0);
-            *reinterpret_cast<float4*>(wlv + 4) = *reinterpret_cast<const float4*>(wl_s + x0 + 4);
-            *reinterpret_cast<float4*>(qv) = *reinterpret_cast<const float4*>(q_s + x0);
-            *reinterpret_cast<float4*>(qv + 4) = *reinterpret_cast<const float4*>(q_s + x0 + 4);
-            *reinterpret_cast<int4*>(lv) = *reinterpret_cast<const int4*>(lab_s + x0);
-            *reinterpret_cast<int4*>(lv + 4) = *reinterpret_cast<const int4*>(lab_s + x0 + 4);
-          }
-#pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            float rr[2];
-#pragma unroll
-            for (int u2 = 0; u2 < 2; ++u2) {
-              const int xe = e + u2;
-              const float a = fmaf(v[q8 + xe], inv, -wv[xe]) - wlv[xe];  // h'' - w >= 1
-              const float p2 = ex2_approx(13.0f - a);                     // (p/2) 2^13
-              rr[u2] = (lv[xe] == i) ? qv[xe] : -p2;
-            }
-            const __half2 h2 = __floats2half2_rn(rr[0], rr[1]);
-            const float2 hf = __half22float2(h2);
-            const __half2 l2 = __floats2half2_rn(rr[0] - hf.x, rr[1] - hf.y);
-            ph[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
-            pl[e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
-          }
-          // 8 consecutive pixels (k) of row tid = one 16-byte core-matrix row
-          const int x0 = half * 32 + q8;
-          const unsigned off = (x0 / 16) * (kTc2Threads * 32) + slab_off(tid, x0 % 16);
-          *reinterpret_cast<uint4*>(smem + L::RH_OFF + off) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
-          *reinterpret_cast<uint4*>(smem + L::RL_OFF + off) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
-        }
-      }
-      sync_tc();
-      if (tid == 0) {
-        const bool fresh = (t % kTc2Flush) == 0;
+      __syncwarp();
+      cs.advance(ntiles);
+    };
+    load_coef(0);
+    if (nlines > 1) load_coef(1);
+    while (cl.n < nitems && cl.n < kTc2Buf - 1) load_next();
+    while (cs.n < nitems && cs.n < kTc2S) issue_s();
+    for (int k = 0; k < nitems; ++k) {
+      const int st = k % kTc2S, b = k % kTc2Buf;
+      mbar_wait(&bar_p[st], (unsigned)(k / kTc2S) & 1u);  // r' of item k is in S_st
+      tc_fence_after();
+      if (leader) {  // UMMA 2: R += [hi hi lo] . [L_hi L_lo L_hi]^T over the 64 pixels
+        const unsigned tr = r_col(cm);
+        const unsigned ts = tmem + 64u * st;
+        const uint64_t dl = d_pix + (uint64_t)((b * L::PIX + KS * (kTc2Px * 32)) >> 4);
+        const bool fresh = cm.t % kTc2Group == 0;
 #pragma unroll
         for (int s = 0; s < 3 * (kTc2Px / 16); ++s) {
           const int p = s / (kTc2Px / 16), ks = s % (kTc2Px / 16);
-          const unsigned a_off = (p < 2 ? L::RH_OFF : L::RL_OFF) + ks * (kTc2Threads * 32);
-          const unsigned b_off = (p == 1 ? L::LL_OFF : L::LH_OFF) + ks * (16 * 32);
-          umma_f16_ss(t_r, umma_desc(sbase + a_off), umma_desc(sbase + b_off), IDESC2,
-                      !(fresh && s == 0));
+          // pixels [16 ks, 16 ks + 16): half ks / 2, packed columns 8 (ks % 2)
+          const unsigned a = ts + 32u * (ks >> 1) + 8u * (ks & 1) + (p == 2 ? 16u : 0u);
+          const uint64_t bo = dl + (uint64_t)(((p == 1 ? (kTc2Px / 16) * 512 : 0) + ks * 512) >> 4);
+          umma_f16_ts(tr, a, bo, IDESC2, !(fresh && s == 0));
         }
-        umma_commit(&mbar);
       }
-      wait_mma();
-      if ((t % kTc2Flush) == kTc2Flush - 1 || t == ntiles - 1) {
-        float v[32];
-        tmem_ld32(t_r + lane_off, v);
-#pragma unroll
-        for (int j = 0; j < J; ++j) R64[j] += (double)v[j];
-        tc_fence_before();
-      }
-    }
-    // R_j = 2 * sum (r/2) L_j = 2 * acc * 2^-(13 + 10): expand into the K rows
-    const double rs = 2.0 / (8192.0 * 1024.0);
-    if (active) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const double prev = line == l0 ? 0.0 : acc[(int64_t)k * g.N];
-        acc[(int64_t)k * g.N] = fma(lc[k], rs * R64[alpha_of(DIM, D, k, DIM - 1)], prev);
+      __syncwarp();
+      cm.advance(ntiles);
+      if (cs.n < nitems)
+        issue_s();  // item k + 3 into the S stage item k just released
+      else if (k == nitems - 1 && leader)
+        umma_commit(&bar_end);
+      if (k + 2 < nitems) {
+        // UMMA 1 of item k + 2 complete => every MMA issued before it, incl. UMMA 2
+        // of item k - 1: its buffer is free; so is a finished line's coefficient image
+        mbar_wait(&bar_s[(k + 2) % kTc2S], (unsigned)((k + 2) / kTc2S) & 1u);
+        if (cl.n < nitems) load_next();
+        for (; cw.n <= k + 2; cw.advance(ntiles))  // every item up to k + 2 is done
+          if (cw.t == ntiles - 1 && cw.li + 2 < nlines) load_coef(cw.li + 2);
       }
     }
+  } else {
+    // ======================= epilogue warps
+    const int q = warp & 3, h = warp >> 2;  // lane quarter, pixel half
+    const int i = gbase + 32 * q + lane;     // this thread's grain (TMEM lane)
+    const bool active = i < g.N;
+    const unsigned lane_off = (unsigned)(32 * q) << 16;
+    double* acc = g.part_g + (int64_t)blockIdx.y * K * g.N + (active ? i : 0);
+    const double rs = -2.0 / (8192.0 * 1024.0);  // R_true = -2 acc 2^-(13 + 10): r' = -r
+    double R64[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) R64[j] = 0.0;
+    auto flush = [&](const Tc2Cursor& c) {  // group of item c complete -> fp64; line -> K rows
+      uint32_t rv[16];
+      tmem_ld16_nowait(r_col(c) + lane_off, rv);
+      tmem_ld_wait();
+      tmem_regs_ready(rv);
+#pragma unroll
+      for (int j = 0; j < J; ++j) R64[j] += (double)__uint_as_float(rv[j]);
+      if (c.t == ntiles - 1) {
+        if (active) {
+          const double* lcp = g.tc_lc + (l0 + c.li) * K;  // k_tc_coeffs
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const double prev = c.li == 0 ? 0.0 : acc[(int64_t)k * g.N];
+            acc[(int64_t)k * g.N] = fma(lcp[k], rs * R64[alpha_of(DIM, D, k, DIM - 1)], prev);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < J; ++j) R64[j] = 0.0;
+      }
+    };
+
+    int sB_next = g.tc_meta[l0 * g.tc_nchunks + blockIdx.x].x;
+    float inv = 0.0f;
+    Tc2Cursor c, cf;  // current item; item whose group may be flushed (lags by kTc2S)
+    for (; c.n < nitems; c.advance(ntiles)) {
+      if (c.t == 0) {
+        inv = ldexpf(1.0f, -(sB_next + 10));  // S * inv = h~''
+        if (c.li + 1 < nlines) sB_next = g.tc_meta[(l0 + c.li + 1) * g.tc_nchunks + blockIdx.x].x;
+      }
+      const int st = c.n % kTc2S, b = c.n % kTc2Buf;
+      const unsigned ts = tmem + 64u * st;
+      const float* rec = reinterpret_cast<const float*>(smem + L::REC_OFF + b * L::REC) + 32 * h;
+      mbar_wait(&bar_s[st], (unsigned)(c.n / kTc2S) & 1u);
+      tc_fence_after();
+      // UMMA 1 of this item follows UMMA 2 of item n - 3: that group may be final
+      if (c.n >= kTc2S) {
+        if (h == 0 && group_last(cf)) flush(cf);
+        cf.advance(ntiles);
+      }
+      uint32_t sv[32];
+      tmem_ld32_nowait(ts + lane_off + 32u * h, sv);
+      mbar_wait(&bar_full[b], (unsigned)(c.n / kTc2Buf) & 1u);  // records visible
+      const int lab_me = reinterpret_cast<const int*>(rec)[3 * kTc2Px + lane];
+      const bool lab_warp = __any_sync(0xffffffffu, (unsigned)(lab_me - (gbase + 32 * q)) < 32u);
+      tmem_ld_wait();
+      tmem_regs_ready(sv);
+      float rr[32];
+#pragma unroll
+      for (int x4 = 0; x4 < 32; x4 += 4) {
+        const float4 w4 = *reinterpret_cast<const float4*>(rec + x4);
+        const float4 l4 = *reinterpret_cast<const float4*>(rec + kTc2Px + x4);
+        const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+        const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)  // p/2 * 2^13 = 2^(13 + w - h~'')
+          rr[x4 + e] = ex2_approx(fmaf(-__uint_as_float(sv[x4 + e]), inv, wv[e]) + lv[e]);
+      }
+      if (lab_warp) {  // label grain: -(1 - p_G)/2 * 2^13 from pass 1 (no cancellation)
+        const int* labs = reinterpret_cast<const int*>(rec) + 3 * kTc2Px;
+        const float* qn = rec + 2 * kTc2Px;
+#pragma unroll
+        for (int x = 0; x < 32; ++x)
+          if (labs[x] == i) rr[x] = qn[x];
+      }
+      uint32_t ph[16], pl[16];
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) {
+        const __half2 h2 = __floats2half2_rn(rr[2 * cc], rr[2 * cc + 1]);
+        const float2 hf = __half22float2(h2);
+        const __half2 l2 = __floats2half2_rn(rr[2 * cc] - hf.x, rr[2 * cc + 1] - hf.y);
+        ph[cc] = *reinterpret_cast<const uint32_t*>(&h2);
+        pl[cc] = *reinterpret_cast<const uint32_t*>(&l2);
+      }
+      tmem_st16(ts + lane_off + 32u * h, ph);
+      tmem_st16(ts + lane_off + 32u * h + 16u, pl);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_p[st]);
+    }
+    // the last groups: complete once the final commit lands
+    mbar_wait(&bar_end, 0);
+    tc_fence_after();
+    for (; cf.n < nitems; cf.advance(ntiles))
+      if (h == 0 && group_last(cf)) flush(cf);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, 128);
+  if (warp == 8) tmem_dealloc(tmem, 256);
 }
 
 }  // namespace pgx
