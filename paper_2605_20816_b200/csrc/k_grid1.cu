@@ -1,0 +1,24 @@
+// k_grid1.cu — regular-grid fp64 pass 1; launchers declared in pgx_launch.cuh.
+#include "pgx_grid.cuh"
+
+namespace pgx {
+
+template <int DIM, int D>
+void grid_dispatch_pass1(const GridParams& g, int R, int blocks, cudaStream_t s) {
+  if (R == 4)
+    k_grid_pass1<DIM, D, 4><<<blocks, kG1Threads, 0, s>>>(g);
+  else if (R == 2)
+    k_grid_pass1<DIM, D, 2><<<blocks, kG1Threads, 0, s>>>(g);
+  else
+    k_grid_pass1<DIM, D, 1><<<blocks, kG1Threads, 0, s>>>(g);
+}
+
+#define PGX_I(DIM, D) template void grid_dispatch_pass1<DIM, D>(const GridParams&, int, int, cudaStream_t);
+// the build may compile this unit several times, each with a subset
+// (build.py: -DPGX_INST_SET=...), so the slow fp64 kernels compile in parallel
+#ifndef PGX_INST_SET
+#define PGX_INST_SET PGX_INST_GRID
+#endif
+PGX_INST_SET(PGX_I)
+
+}  // namespace pgx

@@ -1,0 +1,38 @@
+// k_tc2.cu — tensor-core pass 2 and the per-evaluation operand tables; launchers declared in pgx_launch.cuh.
+#include "pgx_grid.cuh"
+
+namespace pgx {
+
+template <int DIM, int D>
+void tc_dispatch_coeffs(const GridParams& g, const GridPlan& gp, cudaStream_t s) {
+  dim3 grid(gp.tc_nchunks, gp.lines);
+  k_tc_coeffs<DIM, D><<<grid, kTcCoefChunk, 0, s>>>(g, gp.tc_coef, gp.tc_img,
+                                                    reinterpret_cast<TcCoefMeta*>(gp.tc_meta),
+                                                    gp.tc_nchunks);
+}
+
+template <int DIM, int D>
+void tc_dispatch_pix(const GridParams& g, const GridPlan& gp, cudaStream_t s) {
+  k_tc_pix<D><<<g.side / kTcPixTile, kTcPixTile, 0, s>>>(g.M, g.legendre, gp.tc_pix);
+}
+
+template <int DIM, int D>
+void tc_dispatch_pass2(const GridParams& g, dim3 grid, cudaStream_t s) {
+  auto kern = k_tc_pass2<DIM, D>;
+  // padded so that <= 2 CTAs (2 x 256 TMEM columns) share an SM
+  const int smem = std::max(TcP2Smem<D + 1>::TOTAL, 80 * 1024);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  kern<<<grid, kTc2Threads, smem, s>>>(g);
+}
+
+#define PGX_I(DIM, D) \
+  template void tc_dispatch_coeffs<DIM, D>(const GridParams&, const GridPlan&, cudaStream_t); \
+  template void tc_dispatch_pix<DIM, D>(const GridParams&, const GridPlan&, cudaStream_t); \
+  template void tc_dispatch_pass2<DIM, D>(const GridParams&, dim3, cudaStream_t);
+PGX_INST_GRID(PGX_I)
+
+}  // namespace pgx

@@ -14,6 +14,8 @@
 #include "pgx_common.cuh"
 #include "pgx_general.cuh"
 #include "pgx_grid.cuh"
+#include "pgx_grid_eval.cuh"
+#include "pgx_launch.cuh"
 
 using namespace pgx;
 
@@ -120,27 +122,7 @@ int sm_count(int device) {
 }
 
 // ------------------------------------------------------------------ dispatch
-template <int DIM, int D>
-void launch_general_pass1(const EvalParams& prm, int blocks, bool eval, cudaStream_t s) {
-  if (eval)
-    k_general_pass1<DIM, D, true><<<blocks, kP1Threads, 0, s>>>(prm);
-  else
-    k_general_pass1<DIM, D, false><<<blocks, kP1Threads, 0, s>>>(prm);
-}
-template <int DIM, int D>
-void launch_general_fixup(const EvalParams& prm, int sms, cudaStream_t s) {
-  k_general_fixup<DIM, D><<<sms, 128, 0, s>>>(prm);
-}
-template <int DIM, int D>
-void launch_general_pass2(const EvalParams& prm, int N, int splits, cudaStream_t s) {
-  dim3 grid((N + kP2Threads - 1) / kP2Threads, splits);
-  k_general_pass2<DIM, D><<<grid, kP2Threads, 0, s>>>(prm);
-}
-template <int DIM, int D>
-void launch_tail(const EvalParams& prm, const TailParams& tp, int blocks, cudaStream_t s) {
-  k_tail<DIM, D><<<blocks, kTailThreads, 0, s>>>(prm, tp);
-}
-
+// (launchers are defined and instantiated in the k_*.cu translation units)
 #define PGX_DEG_SWITCH2(FN, ...)                 \
   switch (pb->degree) {                          \
     case 0: FN<2, 0>(__VA_ARGS__); break;        \

@@ -314,7 +314,7 @@ struct ReduceParams {
 };
 
 // grad = -(sum over splits, fixed order) / (eps P) - lambda theta (free columns)
-__global__ void __launch_bounds__(256) k_reduce_grad(ReduceParams prm) {
+static __global__ void __launch_bounds__(256) k_reduce_grad(ReduceParams prm) {
   const int64_t KN = (int64_t)prm.K * prm.N;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < KN;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -347,7 +347,7 @@ struct StatsDev {
   long long n_points, n_correct, n_ambiguous, n_nonfinite;
 };
 
-__global__ void __launch_bounds__(256) k_finalize(FinalParams prm) {
+static __global__ void __launch_bounds__(256) k_finalize(FinalParams prm) {
   __shared__ double rd[256];
   __shared__ long long ri[256];
   const int tid = threadIdx.x;
@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(EvalParams e, TailParams 
 }
 
 // theta (fp32 or fp64) -> fp64 working copy
-__global__ void k_theta_to_f64(const void* __restrict__ src, int is_f32, int64_t n,
+static __global__ void k_theta_to_f64(const void* __restrict__ src, int is_f32, int64_t n,
                                double* __restrict__ dst) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x)

@@ -157,216 +157,10 @@ inline cudaError_t grid_plan_create(GridPlan& gp, const pgx_desc* d, int sms, si
   return cudaSuccess;
 }
 
-template <int DIM, int D>
-inline void grid_dispatch_pass1(const GridParams& g, int R, int blocks, cudaStream_t s) {
-  if (R == 4)
-    k_grid_pass1<DIM, D, 4><<<blocks, kG1Threads, 0, s>>>(g);
-  else if (R == 2)
-    k_grid_pass1<DIM, D, 2><<<blocks, kG1Threads, 0, s>>>(g);
-  else
-    k_grid_pass1<DIM, D, 1><<<blocks, kG1Threads, 0, s>>>(g);
-}
+}  // namespace pgx
 
-template <int DIM, int D, int R>
-inline void launch_tc_pass1_r(const GridParams& g, int blocks, cudaStream_t s) {
-  auto kern = k_tc_pass1<DIM, D, R>;
-  // padded so that <= 4 CTAs (4 x 128 TMEM columns) share an SM
-  const int smem = std::max(TcP1Smem<D + 1, R>::TOTAL, kTcMinSmem);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    configured = true;
-  }
-  kern<<<blocks, kTcThreads, smem, s>>>(g);
-}
+#include "pgx_launch.cuh"
 
-template <int DIM, int D>
-inline void tc_dispatch_pass1(const GridParams& g, int R, int blocks, cudaStream_t s) {
-  if (R == 4)
-    launch_tc_pass1_r<DIM, D, 4>(g, blocks, s);
-  else if (R == 2)
-    launch_tc_pass1_r<DIM, D, 2>(g, blocks, s);
-  else
-    launch_tc_pass1_r<DIM, D, 1>(g, blocks, s);
-}
-
-template <int DIM, int D>
-inline void tc_dispatch_coeffs(const GridParams& g, const GridPlan& gp, cudaStream_t s) {
-  dim3 grid(gp.tc_nchunks, gp.lines);
-  k_tc_coeffs<DIM, D><<<grid, kTcCoefChunk, 0, s>>>(g, gp.tc_coef, gp.tc_img,
-                                                    reinterpret_cast<TcCoefMeta*>(gp.tc_meta),
-                                                    gp.tc_nchunks);
-}
-
-template <int DIM, int D>
-inline void tc_dispatch_pix(const GridParams& g, const GridPlan& gp, cudaStream_t s) {
-  k_tc_pix<D><<<g.side / kTcPixTile, kTcPixTile, 0, s>>>(g.M, g.legendre, gp.tc_pix);
-}
-
-template <int DIM, int D>
-inline void tc_dispatch_pass2(const GridParams& g, dim3 grid, cudaStream_t s) {
-  auto kern = k_tc_pass2<DIM, D>;
-  // padded so that <= 2 CTAs (2 x 256 TMEM columns) share an SM
-  const int smem = std::max(TcP2Smem<D + 1>::TOTAL, 80 * 1024);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    configured = true;
-  }
-  kern<<<grid, kTc2Threads, smem, s>>>(g);
-}
-
-template <int DIM, int D, int GT>
-inline void launch_grid_pass2_gt(const GridParams& g, dim3 grid, int smem, cudaStream_t s) {
-  auto kern = k_grid_pass2<DIM, D, GT>;
-  static bool configured = false;  // static + dynamic shared memory may exceed 48 KB
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    configured = true;
-  }
-  kern<<<grid, kG2Threads, smem, s>>>(g);
-}
-
-template <int DIM, int D>
-inline void grid_dispatch_pass2(const GridParams& g, int GT, dim3 grid, int smem, cudaStream_t s) {
-  if (GT == 32)
-    launch_grid_pass2_gt<DIM, D, 32>(g, grid, smem, s);
-  else if (GT == 64)
-    launch_grid_pass2_gt<DIM, D, 64>(g, grid, smem, s);
-  else
-    launch_grid_pass2_gt<DIM, D, 128>(g, grid, smem, s);
-}
-
-#define PGX_GRID_DEG(DIM_, FN, ...)              \
-  switch (gp.D) {                                \
-    case 0: FN<DIM_, 0>(__VA_ARGS__); break;     \
-    case 1: FN<DIM_, 1>(__VA_ARGS__); break;     \
-    case 2: FN<DIM_, 2>(__VA_ARGS__); break;     \
-    case 3: FN<DIM_, 3>(__VA_ARGS__); break;     \
-    case 4: FN<DIM_, 4>(__VA_ARGS__); break;     \
-    case 5: FN<DIM_, 5>(__VA_ARGS__); break;     \
-    case 6: FN<DIM_, 6>(__VA_ARGS__); break;     \
-    case 7: FN<DIM_, 7>(__VA_ARGS__); break;     \
-    default: FN<DIM_, 8>(__VA_ARGS__); break;    \
-  }
-#define PGX_GRID_DEG3(FN, ...)                   \
-  switch (gp.D) {                                \
-    case 0: FN<3, 0>(__VA_ARGS__); break;        \
-    case 1: FN<3, 1>(__VA_ARGS__); break;        \
-    case 2: FN<3, 2>(__VA_ARGS__); break;        \
-    case 3: FN<3, 3>(__VA_ARGS__); break;        \
-    default: FN<3, 4>(__VA_ARGS__); break;       \
-  }
-
-struct GridProf {
-  void* ctx;
-  void (*begin)(void*, const char*);
-  void (*end)(void*);
-};
-
-inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool want_grad,
-                            cudaStream_t s, int* launches, int* blocks1, const GridProf& prof) {
-  (void)prec;
-  GridParams g{};
-  g.P = e.P;
-  g.N = e.N;
-  g.M = e.M;
-  g.side = 2 * e.M;
-  g.legendre = e.legendre;
-  g.R = gp.R;
-  g.lines = gp.lines;
-  g.segs = gp.segs;
-  g.theta = e.theta;
-  g.labels = e.labels;
-  g.eps = e.eps;
-  g.c = 1.4426950408889634074 / e.eps;
-  g.tau_amb = e.tau_amb;
-  g.pix_m = e.pix_m;
-  g.pix_w = gp.pix_w;
-  g.pix_q = gp.pix_q;
-  g.part_d = e.part_d;
-  g.part_i = e.part_i;
-  g.fix_count = e.fix_count;
-  g.fix_list = e.fix_list;
-  g.GT = gp.GT;
-  g.lines_per_split = gp.lines_per_split;
-  g.splits = gp.splits;
-  g.part_g = gp.part_out;
-  g.tc_coef = gp.tc_coef;
-  g.tc_img = gp.tc_img;
-  g.tc_meta = gp.tc_meta;
-  g.tc_nchunks = gp.tc_nchunks;
-  g.tc_pix = gp.tc_pix;
-  g.tc_lc = gp.tc_lc;
-  g.tc_rec = want_grad ? gp.tc_rec : nullptr;
-  if (gp.tc && gp.tc_pix && !gp.tc_pix_ready) {  // once per problem
-    if (gp.dim == 2) {
-      PGX_GRID_DEG(2, tc_dispatch_pix, g, gp, s)
-    } else {
-      PGX_GRID_DEG3(tc_dispatch_pix, g, gp, s)
-    }
-    ++*launches;
-    if (cudaPeekAtLastError() != cudaSuccess) return PGX_ERR_CUDA;
-    gp.tc_pix_ready = true;
-  }
-  if (gp.tc) {
-    prof.begin(prof.ctx, "tc_coeffs");
-    if (gp.dim == 2) {
-      PGX_GRID_DEG(2, tc_dispatch_coeffs, g, gp, s)
-    } else {
-      PGX_GRID_DEG3(tc_dispatch_coeffs, g, gp, s)
-    }
-    prof.end(prof.ctx);
-    ++*launches;
-    g.R = gp.tcR;
-    g.segs = gp.tc_segs;
-    prof.begin(prof.ctx, "tc_pass1");
-    if (gp.dim == 2) {
-      PGX_GRID_DEG(2, tc_dispatch_pass1, g, gp.tcR, gp.tc_blocks, s)
-    } else {
-      PGX_GRID_DEG3(tc_dispatch_pass1, g, gp.tcR, gp.tc_blocks, s)
-    }
-    prof.end(prof.ctx);
-    g.R = gp.R;
-    g.segs = gp.segs;
-  } else {
-    prof.begin(prof.ctx, "grid_pass1");
-    if (gp.dim == 2) {
-      PGX_GRID_DEG(2, grid_dispatch_pass1, g, gp.R, gp.blocks1, s)
-    } else {
-      PGX_GRID_DEG3(grid_dispatch_pass1, g, gp.R, gp.blocks1, s)
-    }
-    prof.end(prof.ctx);
-  }
-  ++*launches;
-  *blocks1 = gp.blocks1;
-  if (cudaPeekAtLastError() != cudaSuccess) return PGX_ERR_CUDA;
-  if (want_grad && gp.tc && gp.tc2_splits > 0) {
-    dim3 grid(gp.tc2_gtiles, gp.tc2_splits);
-    g.lines_per_split = gp.tc2_lps;
-    g.splits = gp.tc2_splits;
-    prof.begin(prof.ctx, "tc_pass2");
-    if (gp.dim == 2) {
-      PGX_GRID_DEG(2, tc_dispatch_pass2, g, grid, s)
-    } else {
-      PGX_GRID_DEG3(tc_dispatch_pass2, g, grid, s)
-    }
-    prof.end(prof.ctx);
-    ++*launches;
-    if (cudaPeekAtLastError() != cudaSuccess) return PGX_ERR_CUDA;
-  } else if (want_grad) {
-    dim3 grid(gp.gtiles, gp.splits);
-    prof.begin(prof.ctx, "grid_pass2");
-    if (gp.dim == 2) {
-      PGX_GRID_DEG(2, grid_dispatch_pass2, g, gp.GT, grid, gp.smem2, s)
-    } else {
-      PGX_GRID_DEG3(grid_dispatch_pass2, g, gp.GT, grid, gp.smem2, s)
-    }
-    prof.end(prof.ctx);
-    ++*launches;
-    if (cudaPeekAtLastError() != cudaSuccess) return PGX_ERR_CUDA;
-  }
-  return PGX_OK;
-}
+namespace pgx {
 
 }  // namespace pgx

@@ -1,0 +1,53 @@
+// pgx_launch.cuh — host-side launchers of every kernel family, declared here
+// and defined + explicitly instantiated in one translation unit per family
+// (k_*.cu), so the families compile in parallel and pgx_api.cu instantiates
+// no kernels itself.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "pgx_general.cuh"
+#include "pgx_grid_common.cuh"
+
+namespace pgx {
+
+struct GridPlan;
+
+// general (any point list) path + tail: pgx_general.cuh
+template <int DIM, int D>
+void launch_general_pass1(const EvalParams& prm, int blocks, bool eval, cudaStream_t s);
+template <int DIM, int D>
+void launch_general_pass2(const EvalParams& prm, int N, int splits, cudaStream_t s);
+template <int DIM, int D>
+void launch_tail(const EvalParams& prm, const TailParams& tp, int blocks, cudaStream_t s);
+
+// regular-grid fp64 path: pgx_grid_pass1.cuh, pgx_grid_pass2.cuh
+template <int DIM, int D>
+void grid_dispatch_pass1(const GridParams& g, int R, int blocks, cudaStream_t s);
+template <int DIM, int D>
+void grid_dispatch_pass2(const GridParams& g, int GT, dim3 grid, int smem, cudaStream_t s);
+
+// tensor-core path: pgx_tc_coeffs.cuh, pgx_tc_pass1.cuh, pgx_tc_pass2.cuh
+template <int DIM, int D>
+void tc_dispatch_coeffs(const GridParams& g, const GridPlan& gp, cudaStream_t s);
+template <int DIM, int D>
+void tc_dispatch_pix(const GridParams& g, const GridPlan& gp, cudaStream_t s);
+template <int DIM, int D>
+void tc_dispatch_pass1(const GridParams& g, int R, int blocks, cudaStream_t s);
+template <int DIM, int D>
+void tc_dispatch_pass2(const GridParams& g, dim3 grid, cudaStream_t s);
+
+}  // namespace pgx
+
+// explicit instantiation over the degrees each path dispatches
+#define PGX_INST_GRID(DECL)                                                         \
+  DECL(2, 0) DECL(2, 1) DECL(2, 2) DECL(2, 3) DECL(2, 4) DECL(2, 5) DECL(2, 6) \
+  DECL(2, 7) DECL(2, 8) DECL(3, 0) DECL(3, 1) DECL(3, 2) DECL(3, 3) DECL(3, 4)
+#define PGX_INST_2D_LO(DECL) DECL(2, 0) DECL(2, 1) DECL(2, 2) DECL(2, 3) DECL(2, 4) DECL(2, 5)
+#define PGX_INST_2D_6(DECL) DECL(2, 6)
+#define PGX_INST_2D_7(DECL) DECL(2, 7)
+#define PGX_INST_2D_8(DECL) DECL(2, 8)
+#define PGX_INST_3D_LO(DECL) DECL(3, 0) DECL(3, 1) DECL(3, 2)
+#define PGX_INST_3D_3(DECL) DECL(3, 3)
+#define PGX_INST_3D_4(DECL) DECL(3, 4)
+#define PGX_INST_GENERAL(DECL) PGX_INST_GRID(DECL) DECL(2, 9) DECL(2, 10)
