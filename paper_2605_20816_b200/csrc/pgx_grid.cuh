@@ -18,7 +18,7 @@ struct GridPlan {
   bool tc = false;  // PGX_PREC_TC: tensor-core pass 1
   int dim = 2, D = 1;
   int R = 1, segs = 1, lines = 0, blocks1 = 0;
-  int tcR = 1, tc_segs = 1, tc_blocks = 0;
+  int tc_blocks = 0;
   int tc2_gtiles = 0, tc2_lps = 1, tc2_splits = 0;  // tensor-core pass 2 (0 = CUDA-core pass 2)
   int part_splits = 0;                             // allocated split slots of part_g
   int tc_nchunks = 0;                              // 128-grain chunks (pgx_tc_coeffs.cuh)
@@ -63,12 +63,10 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
   // 128 pixels share each chunk's coefficient build
   gp.tc = d->precision == PGX_PREC_TC;
   if (gp.tc) {
-    // shared memory per CTA must stay <= ~56 KB for 4 CTAs per SM
-    int tr = std::min(tc_ksteps(d->degree + 1) == 1 ? 4 : 2, side / 128);
-    while (tr > 1 && (int64_t)gp.lines * (side / (128 * tr)) < 4 * sms) tr /= 2;
-    gp.tcR = tr;
-    gp.tc_segs = side / (128 * tr);
-    gp.tc_blocks = gp.lines * gp.tc_segs;
+    // tensor-core pass 1: persistent, one CTA per SM, items of kT1Slots tiles
+    const int64_t ntiles = (int64_t)gp.lines * (side / kTcThreadsTile);
+    const int64_t items = (ntiles + kT1Slots - 1) / kT1Slots;
+    gp.tc_blocks = (int)std::min<int64_t>(items, sms);
     gp.blocks1 = gp.tc_blocks;
   }
   const int N = d->n_grains;

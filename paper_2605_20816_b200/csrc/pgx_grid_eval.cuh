@@ -3,6 +3,8 @@
 // k_*.cu units do not implicitly instantiate each other's launchers).
 #pragma once
 
+#include <cstdlib>
+
 #include "pgx_grid.cuh"
 #include "pgx_launch.cuh"
 
@@ -52,6 +54,10 @@ inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool wa
   g.eps = e.eps;
   g.c = 1.4426950408889634074 / e.eps;
   g.tau_amb = e.tau_amb;
+  {
+    static const int dbg = getenv("PGX_DBG") ? atoi(getenv("PGX_DBG")) : 0;
+    g.dbg = dbg;
+  }
   g.pix_m = e.pix_m;
   g.pix_w = gp.pix_w;
   g.pix_q = gp.pix_q;
@@ -89,17 +95,13 @@ inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool wa
     }
     prof.end(prof.ctx);
     ++*launches;
-    g.R = gp.tcR;
-    g.segs = gp.tc_segs;
     prof.begin(prof.ctx, "tc_pass1");
     if (gp.dim == 2) {
-      PGX_GRID_DEG(2, tc_dispatch_pass1, g, gp.tcR, gp.tc_blocks, s)
+      PGX_GRID_DEG(2, tc_dispatch_pass1, g, gp.tc_blocks, s)
     } else {
-      PGX_GRID_DEG3(tc_dispatch_pass1, g, gp.tcR, gp.tc_blocks, s)
+      PGX_GRID_DEG3(tc_dispatch_pass1, g, gp.tc_blocks, s)
     }
     prof.end(prof.ctx);
-    g.R = gp.R;
-    g.segs = gp.segs;
   } else {
     prof.begin(prof.ctx, "grid_pass1");
     if (gp.dim == 2) {

@@ -33,7 +33,7 @@ void tc_dispatch_coeffs(const GridParams& g, const GridPlan& gp, cudaStream_t s)
 template <int DIM, int D>
 void tc_dispatch_pix(const GridParams& g, const GridPlan& gp, cudaStream_t s);
 template <int DIM, int D>
-void tc_dispatch_pass1(const GridParams& g, int R, int blocks, cudaStream_t s);
+void tc_dispatch_pass1(const GridParams& g, int blocks, cudaStream_t s);
 template <int DIM, int D>
 void tc_dispatch_pass2(const GridParams& g, dim3 grid, cudaStream_t s);
 

@@ -111,8 +111,9 @@ __global__ void __launch_bounds__(kTcCoefChunk) k_tc_coeffs(GridParams g, double
 // the column only, so one table serves every line; built once per problem):
 //   [0, KS*2048)          UMMA 1 B: 64 rows (pixels) x K, pattern [hi, hi, lo]
 //                         of the 2^10-scaled fp16 split of u_j(x)
-//   [KS*2048, +2048)      UMMA 2 B, hi: 16 rows (j, zero-padded) x K = 64 pixels
-//   [KS*2048+2048, +2048) UMMA 2 B, lo
+//   [KS*2048, +4096)      UMMA 2 B: 32 rows x K = 64 pixels, rows 0-15 = L_hi(j),
+//                         rows 16-31 = L_lo(j) (zero-padded j), one 1 KB slab per
+//                         16 pixels
 constexpr int kTcPixTile = 64;
 
 template <int J>
@@ -146,13 +147,12 @@ __global__ void __launch_bounds__(kTcPixTile) k_tc_pix(int M, int legendre,
     *reinterpret_cast<uint4*>(slab + slab_off(tid, 0)) = *reinterpret_cast<const uint4*>(row);
     *reinterpret_cast<uint4*>(slab + slab_off(tid, 8)) = *reinterpret_cast<const uint4*>(row + 8);
   }
-  unsigned char* lh = dst + KS * (kTcPixTile * 32);
-  unsigned char* ll = lh + (kTcPixTile / 16) * 16 * 32;
+  unsigned char* l2 = dst + KS * (kTcPixTile * 32);
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    const unsigned off = (tid / 16) * (16 * 32) + slab_off(j, tid % 16);
-    *reinterpret_cast<__half*>(lh + off) = j < J ? hi[j] : __float2half(0.0f);
-    *reinterpret_cast<__half*>(ll + off) = j < J ? lo[j] : __float2half(0.0f);
+    unsigned char* slab = l2 + (tid / 16) * (32 * 32);
+    *reinterpret_cast<__half*>(slab + slab_off(j, tid % 16)) = j < J ? hi[j] : __float2half(0.0f);
+    *reinterpret_cast<__half*>(slab + slab_off(16 + j, tid % 16)) = j < J ? lo[j] : __float2half(0.0f);
   }
 }
 

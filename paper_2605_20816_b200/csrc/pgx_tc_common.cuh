@@ -40,6 +40,43 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
     if (spin == (1u << 26)) __trap();
   }
 }
+// Same, with a suspend-time hint: the waiting warp sleeps in the barrier
+// unit until the phase completes (or the hint expires) instead of spinning on
+// issue slots the epilogue warps need.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) {
+  const unsigned addr = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  for (unsigned spin = 0;; ++spin) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity), "r"(1000000u)
+        : "memory");
+    if (done) return;
+    if (spin == (1u << 22)) __trap();
+  }
+}
+// the same on a precomputed shared-memory address
+__device__ __forceinline__ void mbar_wait_addr(unsigned addr, unsigned parity) {
+  unsigned done = 0;
+  for (unsigned spin = 0;; ++spin) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(32);
+    if (spin == (1u << 30)) __trap();
+  }
+}
+__device__ __forceinline__ void mbar_arrive_addr(unsigned addr) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
+}
 // arrive once and expect `bytes` more transaction bytes in the current phase
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
@@ -161,6 +198,30 @@ __device__ __forceinline__ void tmem_st16(unsigned taddr, const uint32_t (&r)[16
 }
 __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// registers written by an async TMEM load become usable after the wait; the
+// empty asm ties every use to it
+template <int N>
+__device__ __forceinline__ void tmem_regs_ready(uint32_t (&r)[N]) {
+#pragma unroll
+  for (int q = 0; q < N; ++q) asm volatile("" : "+r"(r[q]));
+}
+__device__ __forceinline__ void tmem_ld32_nowait(unsigned taddr, uint32_t (&s0)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(s0[0]), "=r"(s0[1]), "=r"(s0[2]), "=r"(s0[3]), "=r"(s0[4]), "=r"(s0[5]), "=r"(s0[6]),
+        "=r"(s0[7]), "=r"(s0[8]), "=r"(s0[9]), "=r"(s0[10]), "=r"(s0[11]), "=r"(s0[12]),
+        "=r"(s0[13]), "=r"(s0[14]), "=r"(s0[15]), "=r"(s0[16]), "=r"(s0[17]), "=r"(s0[18]),
+        "=r"(s0[19]), "=r"(s0[20]), "=r"(s0[21]), "=r"(s0[22]), "=r"(s0[23]), "=r"(s0[24]),
+        "=r"(s0[25]), "=r"(s0[26]), "=r"(s0[27]), "=r"(s0[28]), "=r"(s0[29]), "=r"(s0[30]),
+        "=r"(s0[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
 }
 
 // ----------------------------------------------------------------- operands

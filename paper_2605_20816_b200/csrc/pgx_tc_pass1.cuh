@@ -1,21 +1,31 @@
 // pgx_tc_pass1.cuh — PGX_PREC_TC pass 1: the logit contraction h'' = L(x_fast)
-// B''(line) (objective.py:99) on the 5th-generation tensor cores, the
-// log-sum-exp / min / arg-min epilogue on the CUDA cores.
+// B''(line) (objective.py:99) on the 5th-generation tensor cores and ONE
+// streaming sweep over the grains per pixel on the CUDA cores: running min,
+// online log-sum-exp (objective.py:102-106) and the arg-min bookkeeping of
+// geometry.py:201-210.
 //
-// CTA = R tiles of 128 pixels of one line (4 warps; thread = TMEM lane = pixel).
-// Grains stream in chunks of 256 = the UMMA N.  Per (chunk, tile) one elected
-// thread issues tc_ksteps(J) tcgen05.mma (M=128, N=256, K=16, fp16 in, fp32
-// accumulate in TMEM) and commits to an mbarrier; the epilogue reads 32-column
-// blocks with tcgen05.ld.  Operands use a 3-product fp16 split (hi*hi + hi*lo
-// + lo*hi): logits carry ~fp32 accuracy, bounded by delta = gamma * max|B''|_1.
+// Persistent, warp-specialised, one CTA per SM (all 512 TMEM columns):
+//   warps 0-15  epilogue: slot s = warp / 4 is one tile of 128 pixels of a
+//               line, lane quarter warp % 4; thread = TMEM lane = pixel;
+//   warp 16     producer: bulk async copies of the per-line coefficient
+//               images (pgx_tc_coeffs.cuh) into a 3-stage ring, and one lane
+//               issuing tcgen05.mma (M = 128 pixels, N = 64 grains, K = 16 *
+//               tc_ksteps(J), fp16 3-product split, fp32 accumulate) into a
+//               double-buffered accumulator per slot, committed to mbarriers.
+// A work item is 4 consecutive tiles (one line when the side has >= 4 tiles,
+// else one tile per line — each slot then has its own coefficient image);
+// items are strided over the CTAs in a fixed order (deterministic partials).
 //
-//   sweep A: m~ = min h~'' (one FMNMX per logit);
-//   sweep B: s' = sum_{i != G} 2^(ref - h~''_i), ref = m~ - delta - 1, one
-//            FFMA + MUFU.EX2 + FADD per logit; logits within 2 delta + tie +
-//            ambiguity band of m~ are re-evaluated exactly in fp64 (vote per
-//            32-column block) for the exact tie-tolerant arg-min
-//            (geometry.py:201-210), min and runner-up.
-// The label term is exact (fp64) and excluded from s'.
+// Epilogue, per 32-column block of one pixel (h~'' = S * inv):
+//   mb = block min (FMNMX3); the two best blocks (b1, b2) and their minima are
+//   tracked per pixel; the reference ref of s' = sum_{i != G} 2^(ref - h~''_i)
+//   moves only when the min falls more than kT1Stale below it (then s' is
+//   rescaled by 2^(ref_old - ref_new)): one FFMA + MUFU.EX2 + FADD per logit.
+// Per pixel at the end: the label term in fp64, and the exact
+//   fp64 tie-tolerant arg-min / min / runner-up over the 32 grains of block b1
+//   — every logit within 2 delta + tie band of the fp32 min lies in b1 unless
+//   the runner-up block is that close too; such pixels (real cross-block ties)
+//   are queued for the exact re-scan of the tail kernel.
 #pragma once
 
 #include "pgx_grid_common.cuh"
@@ -24,12 +34,17 @@
 
 namespace pgx {
 
-constexpr int kTcThreads = 128;
-constexpr int kTcChunk = 128;     // grains per chunk (UMMA N)
-constexpr int kTcTmemCols = 128;  // one fp32 accumulator tile: 4 CTAs share an SM's TMEM
-constexpr int kTcMinSmem = 46 * 1024;  // keeps residency at <= 4 CTAs per SM
+constexpr int kTcThreadsTile = 128;              // pixels per tile (UMMA M, TMEM lanes)
+constexpr int kT1Slots = 4;                      // pixel tiles per item
+constexpr int kT1EpiWarps = 4 * kT1Slots;        // 16
+constexpr int kT1Threads = 32 * kT1EpiWarps + 32;  // + producer warp
+constexpr int kT1Cols = 32;                      // grains per MMA (UMMA N) = one block
+constexpr int kT1Bufs = 4;                       // accumulator buffers per slot (TMEM)
+constexpr int kT1Ring = 16;                      // coefficient image ring (images in flight)
+constexpr float kT1Stale = 24.0f;                // ref may lag the min by this (log2 units)
+constexpr int kT1MinSmem = 120 * 1024;           // one CTA per SM (owns all of TMEM)
 
-// exact per-pixel state for near-minimal logits (shared memory)
+// exact per-pixel state for near-minimal logits
 struct TcRare {
   double m, m2, hb0, hb1;
   int b0, b1, cnt, flags;  // flags: 1 dirty (candidate list overflowed), 2 needfix
@@ -71,282 +86,361 @@ __device__ __forceinline__ void tc_rare_update(TcRare& st, int i, double h, doub
   }
 }
 
-template <int J, int R>
+template <int J>
 struct TcP1Smem {
   static constexpr int KS = tc_ksteps(J);
-  static constexpr int A_BYTES = R * KS * kTcThreads * 32;
-  static constexpr int B_BYTES = KS * kTcChunk * 32;
-  static constexpr int BD_BYTES = 0;  // exact B'' is read from the per-line table
-  static constexpr int RARE_BYTES = R * kTcThreads * (int)sizeof(TcRare);
+  static constexpr int A_SLOT = KS * kTcThreadsTile * 32;  // one 128-row pixel operand
+  static constexpr int IMG = tc_img_bytes<J>();
   static constexpr int A_OFF = 0;
-  static constexpr int B_OFF = A_OFF + A_BYTES;
-  static constexpr int BD_OFF = B_OFF + B_BYTES;
-  static constexpr int RARE_OFF = BD_OFF + BD_BYTES;
-  static constexpr int TOTAL = RARE_OFF + RARE_BYTES;
+  static constexpr int IMG_OFF = A_OFF + kT1Slots * A_SLOT;
+  static constexpr int RING = (200 * 1024 - IMG_OFF) / IMG < kT1Ring ? (200 * 1024 - IMG_OFF) / IMG : kT1Ring;
+  static constexpr int TOTAL = IMG_OFF + RING * IMG;
 };
 
-template <int DIM, int D, int R>
-__global__ void __launch_bounds__(kTcThreads, 4) k_tc_pass1(GridParams g) {
+// exact scan of one 32-grain block of a pixel (fixed order, tc_rare_update);
+// logits in groups of 8 so their coefficient loads are in flight together
+template <int J>
+__device__ __forceinline__ void tc_exact_block(TcRare& st, const double* coef_line, int blk, int N,
+                                               const double* u, double c) {
+  const int i0 = blk * 32, i1 = min(N, i0 + 32);
+  for (int ib = i0; ib < i1; ib += 8) {
+    double h[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) h[k] = ib + k < i1 ? eval_line<J>(coef_line + (int64_t)(ib + k) * J, u) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (ib + k < i1) tc_rare_update(st, ib + k, h[k], c);
+  }
+}
+
+// named barrier of the 4 warps (128 threads) of one slot
+__device__ __forceinline__ void slot_sync(int s) {
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + s) : "memory");
+}
+
+template <int DIM, int D>
+__global__ void __launch_bounds__(kT1Threads, 1) k_tc_pass1(GridParams g) {
   constexpr int J = D + 1;
-  constexpr int K = feature_count(DIM, D);
-  using L = TcP1Smem<J, R>;
+  using L = TcP1Smem<J>;
   constexpr int KS = L::KS;
-  constexpr uint32_t IDESC = umma_idesc_f16(128, kTcChunk);
+  constexpr int QB = kTcCoefChunk / kT1Cols;  // blocks per coefficient image
+  constexpr uint32_t IDESC = umma_idesc_f16(128, kT1Cols);
   extern __shared__ __align__(1024) unsigned char smem[];
-  unsigned char* A_s = smem + L::A_OFF;
-  unsigned char* B_s = smem + L::B_OFF;
-  TcRare* rare = reinterpret_cast<TcRare*>(smem + L::RARE_OFF);  // [R][128]
-  __shared__ double lc[K];
-  __shared__ uint64_t mbar;
+  __shared__ uint64_t bar_full[kT1Slots][kT1Bufs];  // MMA of a slot's buffer complete
+  __shared__ uint64_t bar_img[kT1Ring], bar_imgfree[kT1Ring];
   __shared__ unsigned tmem_base;
-  __shared__ unsigned s_bmax;     // max over grains of sum_j |B''_j| (float bits)
-  __shared__ double red_d[kTcThreads];
-  __shared__ long long red_i[kTcThreads];
+  __shared__ double red_d[kT1EpiWarps][2];
+  __shared__ long long red_i[kT1EpiWarps][3];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t line = blockIdx.x / g.segs;
-  const int seg = blockIdx.x % g.segs;
-  const int64_t pbase = line * g.side + (int64_t)seg * kTcThreads * R;
   const int N = g.N;
   const double c = g.c;
+  const int tpl = g.side / kTcThreadsTile;  // tiles per line
+  const int64_t ntiles = (int64_t)g.lines * tpl;
+  const int64_t nitems = (ntiles + kT1Slots - 1) / kT1Slots;
+  const int nimg = (N + kTcCoefChunk - 1) / kTcCoefChunk;
+  const int nblk = (N + kT1Cols - 1) / kT1Cols;
 
-  if (warp == 0) tmem_alloc(&tmem_base, kTcTmemCols);
-  if (tid == 0) {
-    double lcr[K];
-    line_factors<DIM, D>(line, g, lcr);
-#pragma unroll
-    for (int k = 0; k < K; ++k) lc[k] = lcr[k];
-    mbar_init(&mbar, 1);
-    fence_mbar_init();
-    s_bmax = 0u;
-  }
-
-  // pixel operands: A'[p][k] = 2^10 L_j(x_fast), k = b J + j, blocks [hi, hi, lo]
-  int lab[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int col = seg * kTcThreads * R + kTcThreads * r + tid;
-    double u[J];
-    axis_table<D>(axis_coord(col, g.M), g.legendre != 0, u);
-    __half hi[J], lo[J];
-#pragma unroll
-    for (int j = 0; j < J; ++j) split_f16(u[j] * 1024.0, hi[j], lo[j]);
-#pragma unroll
-    for (int k = 0; k < 16 * KS; ++k) {
-      const int b = k / J, j = k % J;
-      const __half val = k < 3 * J ? (b < 2 ? hi[j] : lo[j]) : __float2half(0.0f);
-      *reinterpret_cast<__half*>(A_s + (r * KS + k / 16) * (kTcThreads * 32) +
-                                 slab_off(tid, k % 16)) = val;
+  if (warp == kT1EpiWarps) tmem_alloc(&tmem_base, 512);
+  if (tid == 32 * kT1EpiWarps) {
+    for (int s = 0; s < kT1Slots; ++s)
+      for (int b = 0; b < kT1Bufs; ++b) mbar_init(&bar_full[s][b], 1);
+    for (int b = 0; b < L::RING; ++b) {
+      mbar_init(&bar_img[b], 1);
+      mbar_init(&bar_imgfree[b], kT1Slots);  // every slot leader releases every image
     }
-    lab[r] = g.labels[pbase + kTcThreads * r + tid];
-    TcRare& st = rare[r * kTcThreads + tid];
-    st.m = CUDART_INF;
-    st.m2 = CUDART_INF;
-    st.cnt = 0;
-    st.flags = 0;
-    st.b0 = st.b1 = -1;
+    fence_mbar_init();
   }
-  fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const unsigned tmem = tmem_base;
-  const unsigned a_addr = (unsigned)__cvta_generic_to_shared(A_s);
-  const unsigned b_addr = (unsigned)__cvta_generic_to_shared(B_s);
-  unsigned phase = 0;
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
 
-  // chunk [c0, c0 + cn): copy the precomputed operand image (pgx_tc_coeffs.cuh)
-  // of this line into B_s; returns 2^-(sB + 10) so that D * this = h~''
-  const double* coef_line = g.tc_coef + line * (int64_t)N * J;  // exact B'' of this line
-  auto build_chunk = [&](int c0, int cn) -> float {
-    (void)cn;
-    __syncthreads();
-    const int64_t ci = line * g.tc_nchunks + c0 / kTcChunk;
-    copy_coef_img<J, kTcThreads>(B_s, g.tc_img + ci * tc_img_bytes<J>(), tid);
-    const int2 m = g.tc_meta[ci];
-    if (tid == 0) atomicMax(&s_bmax, (unsigned)m.y);  // non-negative float bits
-    fence_proxy_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    return ldexpf(1.0f, -(m.x + 10));
-  };
-
-  // one UMMA tile: D[128 x 256] = A_r B^T, then wait for the accumulator
-  auto mma_tile = [&](int r) {
-    if (tid == 0) {
-#pragma unroll
-      for (int s = 0; s < KS; ++s)
-        umma_f16_ss(tmem, umma_desc(a_addr + (r * KS + s) * (kTcThreads * 32)),
-                    umma_desc(b_addr + s * (kTcChunk * 32)), IDESC, s > 0);
-      umma_commit(&mbar);
+  // the images of a chunk: one per distinct line among the item's tiles;
+  // js[s] = index of slot s's image, returns the count
+  auto distinct = [&](int64_t it, int (&js)[kT1Slots]) {
+    const int64_t t0 = it * kT1Slots;
+    int n = 0;
+    for (int s = 0; s < kT1Slots; ++s) {
+      if (s > 0 && t0 + s < ntiles && (t0 + s) / tpl == (t0 + s - 1) / tpl)
+        js[s] = js[s - 1];
+      else
+        js[s] = t0 + s < ntiles ? n++ : 0;
     }
-    mbar_wait(&mbar, phase);
-    phase ^= 1u;
-    tc_fence_after();
+    return n;
   };
-  const unsigned trow = tmem + ((unsigned)(warp * 32) << 16);
 
-  // ---------------------------------------------------------------- sweep A
-  // Per-tile state lives in small arrays indexed by the (rolled) tile loop:
-  // a few local-memory accesses per tile instead of R copies of the epilogue
-  // code (the unrolled version thrashed the instruction cache).
-  float mt[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) mt[r] = CUDART_INF_F;
-  for (int c0 = 0; c0 < N; c0 += kTcChunk) {
-    const int cn = min(kTcChunk, N - c0);
-    const float inv = build_chunk(c0, cn);
-#pragma unroll 1
-    for (int r = 0; r < R; ++r) {
-      mma_tile(r);
-      float m0 = CUDART_INF_F, m1 = CUDART_INF_F;
-      for (int cb = 0; cb < cn; cb += 32) {
-        float v[32];
-        tmem_ld32(trow + cb, v);
-        if (cb + 32 <= cn) {
-#pragma unroll
-          for (int q = 0; q < 32; q += 2) {
-            m0 = fminf(m0, v[q]);
-            m1 = fminf(m1, v[q + 1]);
+  if (warp == kT1EpiWarps) {
+    // ============================ loader warp: every image of every item of
+    // this CTA, in consumption order, into a RING-deep ring; a ring slot is
+    // refilled once all four slot leaders released its previous image
+    const bool leader = lane == 0;
+    int gl = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+      int js[kT1Slots];
+      const int nl = distinct(it, js);
+      for (int ci = 0; ci < nimg; ++ci)
+        for (int j = 0; j < nl; ++j, ++gl) {
+          const int slot = gl % L::RING;
+          mbar_wait(&bar_imgfree[slot], (unsigned)((gl / L::RING) & 1) ^ 1u);
+          if (leader) {
+            int s = 0;
+            while (js[s] != j) ++s;  // first tile slot of distinct line j
+            const int64_t line = (it * kT1Slots + s) / tpl;
+            mbar_arrive_expect_tx(&bar_img[slot], L::IMG);
+            bulk_g2s(smem + L::IMG_OFF + slot * L::IMG,
+                     g.tc_img + (line * g.tc_nchunks + ci) * (int64_t)L::IMG, L::IMG, &bar_img[slot]);
           }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 32; ++q)
-            if (cb + q < cn) m0 = fminf(m0, v[q]);
+          __syncwarp();
         }
+    }
+  } else {
+    // ============================ epilogue warps: thread = pixel of slot s;
+    // the slot's 4 warps meet at a named barrier after every TMEM load and the
+    // slot leader (lane 0 of warp 4s) issues the MMA that refills the buffer
+    const int s = warp >> 2, q = warp & 3;
+    const bool leader = q == 0 && lane == 0;
+    const unsigned lane_off = (unsigned)(32 * q) << 16;
+    const int prow = 32 * q + lane;  // row of the slot's 128-pixel tile
+    const unsigned t_slot = tmem + lane_off + (unsigned)(s * kT1Bufs * kT1Cols);
+    const unsigned a_full = (unsigned)__cvta_generic_to_shared(&bar_full[s][0]);
+    const unsigned a_slot = sbase + L::A_OFF + (unsigned)(s * KS * (kTcThreadsTile * 32));
+    double ell = 0.0, e0 = 0.0;
+    long long correct = 0, amb = 0, nonfinite = 0;
+    int rc = 0;  // rounds (blocks) of this slot so far: buffer rc % kT1Bufs, phase (rc / kT1Bufs) & 1
+    int gc = 0;  // images released so far (leader only; all slots walk the same image sequence)
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+      int js[kT1Slots];
+      const int nl = distinct(it, js);
+      const int64_t tile = it * kT1Slots + s;
+      const bool active = tile < ntiles;
+      const int64_t line = active ? tile / tpl : 0;
+      const int col = (int)(tile % tpl) * kTcThreadsTile + prow;
+      if (active) {  // pixel operand row: A'[p][k] = 2^10 L_j(x_fast), k = b J + j, blocks [hi, hi, lo]
+        double u[J];
+        axis_table<D>(axis_coord(col, g.M), g.legendre != 0, u);
+        __half hi[J], lo[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) split_f16(u[j] * 1024.0, hi[j], lo[j]);
+        unsigned char* A_s = smem + L::A_OFF + s * L::A_SLOT;
+#pragma unroll
+        for (int k = 0; k < 16 * KS; ++k) {
+          const int b = k / J, j = k % J;
+          const __half val = k < 3 * J ? (b < 2 ? hi[j] : lo[j]) : __float2half(0.0f);
+          *reinterpret_cast<__half*>(A_s + (k / 16) * (kTcThreadsTile * 32) + slab_off(prow, k % 16)) = val;
+        }
+        fence_proxy_async_smem();
       }
-      mt[r] = fminf(mt[r], fminf(m0, m1) * inv);
-      tc_fence_before();
-      __syncthreads();
-      tc_fence_after();
-    }
-  }
-  const float bnorm = __uint_as_float(s_bmax);
-  // |h~'' - h''| <= delta: fp16 split (2^-21 relative per operand pair) plus
-  // the fp32 accumulation of 3J products; generous factor 2
-  const float delta = 2.0f * (4.7683716e-07f + 3 * J * 5.9604645e-08f) * bnorm + 1e-30f;
-
-  // ---------------------------------------------------------------- sweep B
-  float ref[R], athr[R], sx[R];
-  double sx64[R];
+      slot_sync(s);
+      // leader: MMA of block kb of this item into buffer (rc0 + kb) % kT1Bufs;
+      // waits for the chunk's images at its first block, releases them after its last
+      const int rc0 = rc;
+      auto issue = [&](int kb) {
+        const int ci = kb / QB, qb = kb % QB;
+        if (qb == 0)
+          for (int j = 0; j < nl; ++j)
+            mbar_wait(&bar_img[(gc + j) % L::RING], (unsigned)(((gc + j) / L::RING) & 1));
+        tc_fence_after();
+        const unsigned buf = (unsigned)((rc0 + kb) % kT1Bufs);
+        const unsigned bimg = sbase + L::IMG_OFF + (unsigned)(((gc + js[s]) % L::RING) * L::IMG) +
+                              (unsigned)(qb * (kT1Cols / 8) * 256);
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    ref[r] = mt[r] - delta - 1.0f;
-    const double band = c * fmax(kTieRtol, g.tau_amb) * (1.0 + fabs((double)mt[r] / c));
-    athr[r] = 1.0f + 3.0f * delta + (float)band * 1.001f;  // a = h~'' - ref <= athr: candidate
-    sx[r] = 0.0f;
-    sx64[r] = 0.0;
-  }
-  for (int c0 = 0; c0 < N; c0 += kTcChunk) {
-    const int cn = min(kTcChunk, N - c0);
-    const float inv = build_chunk(c0, cn);
-#pragma unroll 1
-    for (int r = 0; r < R; ++r) {
-      mma_tile(r);
-      const int labc = lab[r] - c0;
-      const float refr = ref[r], athrr = athr[r];
-      double sxr = sx64[r];
-      for (int cb = 0; cb < cn; cb += 32) {
-        float v[32];
-        tmem_ld32(trow + cb, v);
-        const bool full = cb + 32 <= cn;
-        const bool lab_here = (unsigned)(labc - cb) < 32u;
-        bool cand = false;
-        float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // 4 independent FADD chains
-        if (full && !__any_sync(0xffffffffu, lab_here)) {
-#pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const float a = fmaf(v[q], inv, -refr);
-            cand |= a <= athrr;
-            s4[q & 3] += ex2_approx(-a);
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const float a = fmaf(v[q], inv, -refr);
-            const bool ok = cb + q < cn;
-            cand |= ok && a <= athrr;
-            const float e = ex2_approx(-a);
-            s4[q & 3] += (ok && cb + q != labc) ? e : 0.0f;
-          }
+        for (int k = 0; k < KS; ++k)
+          umma_f16_ss(tmem + (unsigned)((s * kT1Bufs + buf) * kT1Cols),
+                      umma_desc(a_slot + k * (kTcThreadsTile * 32)), umma_desc(bimg + k * (kTcCoefChunk * 32)),
+                      IDESC, k > 0);
+        umma_commit(&bar_full[s][buf]);
+        if (qb == QB - 1 || kb == nblk - 1) {
+          for (int j = 0; j < nl; ++j) umma_commit(&bar_imgfree[(gc + j) % L::RING]);
+          gc += nl;
         }
-        sxr += (double)((s4[0] + s4[1]) + (s4[2] + s4[3]));
-        if (__any_sync(0xffffffffu, cand)) {
-          // exact fp64 re-evaluation of the near-minimal logits: collect the
-          // candidate columns as a bit mask (static register indices), then
-          // walk the set bits
-          unsigned cm = 0u;
-#pragma unroll
-          for (int q = 0; q < 32; ++q)
-            if (fmaf(v[q], inv, -refr) <= athrr && cb + q < cn) cm |= 1u << q;
-          if (cm) {
-            const int col = seg * kTcThreads * R + kTcThreads * r + tid;
-            double u[J];
-            axis_table<D>(axis_coord(col, g.M), g.legendre != 0, u);
-            TcRare& st = rare[r * kTcThreads + tid];
-            while (cm) {
-              const int q = __ffs(cm) - 1;
-              cm &= cm - 1u;
-              tc_rare_update(st, c0 + cb + q,
-                             eval_line<J>(coef_line + (int64_t)(c0 + cb + q) * J, u), c);
+      };
+      if (!active) {  // empty slot of the last item: release the images, nothing else
+        if (leader)
+          for (int ci = 0; ci < nimg; ++ci) {
+            for (int j = 0; j < nl; ++j) {
+              mbar_wait(&bar_img[(gc + j) % L::RING], (unsigned)(((gc + j) / L::RING) & 1));
+              mbar_arrive(&bar_imgfree[(gc + j) % L::RING]);
             }
+            gc += nl;
+          }
+        continue;
+      }
+      if (leader)
+        for (int kb = 0; kb < min(kT1Bufs, nblk); ++kb) issue(kb);
+      const int64_t p = line * g.side + col;
+      const int lab = g.labels[p];
+      const double* coef_line = g.tc_coef + line * (int64_t)N * J;
+      const int2* meta = g.tc_meta + line * g.tc_nchunks;
+      float ref = CUDART_INF_F, m1 = CUDART_INF_F, m2b = CUDART_INF_F, bmax = 0.0f;
+      int b1 = 0, b2 = 0;
+      unsigned mask1 = 0u;          // columns of block b1 within the candidate window of its min
+      float sx = 0.0f, sxc = 0.0f;  // Kahan-compensated sum of the block sums
+      float inv = 0.0f, dblk = 0.0f;
+      const double bandr = c * fmax(kTieRtol, g.tau_amb);
+      // one 32-grain block: wait, load, refill, min bookkeeping, exponentials
+      auto block = [&](int kb, int cn) {
+        const unsigned buf = (unsigned)(rc % kT1Bufs);
+        if (kb % QB == 0) {
+          const int2 mt = __ldg(meta + kb / QB);
+          inv = __int_as_float((127 - (mt.x + 10)) << 23);  // 2^-(sB + 10): S * inv = h~''
+          const float bn = __int_as_float(mt.y);
+          bmax = fmaxf(bmax, bn);
+          dblk = 2.0f * (4.7683716e-07f + 3 * J * 5.9604645e-08f) * bn + 1e-30f;
+        }
+        mbar_wait_addr(a_full + 8u * buf, (unsigned)((rc / kT1Bufs) & 1));
+        tc_fence_after();
+        uint32_t r0[32];
+        tmem_ld32_nowait(t_slot + buf * kT1Cols, r0);
+        tmem_ld_wait();
+        tmem_regs_ready(r0);
+        tc_fence_before();
+        slot_sync(s);
+        if (leader && kb + kT1Bufs < nblk) issue(kb + kT1Bufs);
+        ++rc;
+        float w[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) w[e] = (cn == 32 || e < cn) ? __uint_as_float(r0[e]) : CUDART_INF_F;
+        // block min: FMNMX3 tree
+        float t11[11];
+#pragma unroll
+        for (int e = 0; e < 10; ++e) t11[e] = fminf(w[3 * e], fminf(w[3 * e + 1], w[3 * e + 2]));
+        t11[10] = fminf(w[30], w[31]);
+        const float mb = fminf(fminf(fminf(t11[0], fminf(t11[1], t11[2])), fminf(t11[3], fminf(t11[4], t11[5]))),
+                               fminf(fminf(t11[6], fminf(t11[7], t11[8])), fminf(t11[9], t11[10])));
+        const float mbs = mb * inv;
+        if (mbs < m2b) {  // top-2 blocks (rare after the first few)
+          if (mbs < m1) {
+            // candidate columns of the new min block: within 2 delta + tie band of its min
+            const float thr = (mbs + 2.0f * dblk + (float)(bandr * (1.0 + fabs((double)mbs / c))) * 1.001f) / inv;
+            unsigned mk = 0u;
+#pragma unroll
+            for (int e = 0; e < 32; ++e) mk |= (w[e] <= thr) ? (1u << e) : 0u;
+            m2b = m1;
+            b2 = b1;
+            m1 = mbs;
+            b1 = kb;
+            mask1 = mk;
+          } else {
+            m2b = mbs;
+            b2 = kb;
+          }
+          if (mbs < ref - kT1Stale) {  // (also the first block: ref = +inf)
+            const float nref = mbs - 1.0f;
+            const double f = exp2((double)nref - (double)ref);
+            sx = (float)((double)sx * f);
+            sxc = (float)((double)sxc * f);
+            ref = nref;
           }
         }
-      }
-      sx64[r] = sxr;
-      tc_fence_before();
-      __syncthreads();
-      tc_fence_after();
-    }
-  }
-
-  // ---------------------------------------------------------- per-pixel finish
-  double ell = 0.0, e0 = 0.0;
-  long long correct = 0, amb = 0, nonfinite = 0;
+        const float nr = -ref;
+        const int labc = lab - kb * kT1Cols;
+        float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // 4 independent FADD chains
+        if (cn == 32 && !__any_sync(0xffffffffu, (unsigned)labc < 32u)) {
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int col = seg * kTcThreads * R + kTcThreads * r + tid;
-    const int64_t p = pbase + kTcThreads * r + tid;
-    double u[J];
-    axis_table<D>(axis_coord(col, g.M), g.legendre != 0, u);
-    const double hG = eval_line<J>(coef_line + (int64_t)lab[r] * J, u);  // same bits as the refine
-    TcRare& st = rare[r * kTcThreads + tid];
-    const double refd = (double)ref[r];
-    const double aG = hG - refd;
-    const double eG = exp2(-aG);
-    const double s = sx64[r] + eG;
-    const double l2s = log2(s);
-    const double l = (-aG - l2s) * 0.69314718055994530942;  // log p_G: objective.py:103-106
-    ell += l;
-    if (!isfinite(l) || !(bnorm <= 3e38f)) nonfinite = 1;
-    if (g.tc_rec) {  // pass-2 record: p_i/2 * 2^13 = 2^(w13 + wl13 - h~''_i)
-      const double w13 = refd - 1.0 - l2s + 13.0;
-      const float wh = (float)w13;
-      float* rec = g.tc_rec + (line * (g.side / kTcPixTile) + (col >> 6)) * (4 * kTcPixTile) + (col & 63);
-      rec[0] = wh;
-      rec[kTcPixTile] = (float)(w13 - (double)wh);
-      rec[2 * kTcPixTile] = (float)(-4096.0 * sx64[r] / s);  // -(1 - p_G)/2 * 2^13
-      reinterpret_cast<int*>(rec)[3 * kTcPixTile] = lab[r];
+          for (int e = 0; e < 32; ++e) s4[e & 3] += ex2_approx(-fmaf(w[e], inv, nr));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float x = ex2_approx(-fmaf(w[e], inv, nr));
+            s4[e & 3] += (e < cn && e != labc) ? x : 0.0f;
+          }
+        }
+        const float y = ((s4[0] + s4[1]) + (s4[2] + s4[3])) - sxc;  // Kahan step
+        const float t = sx + y;
+        sxc = (t - sx) - y;
+        sx = t;
+      };
+      const int nfull = N / kT1Cols;  // full blocks; a partial one follows if N % 32
+#pragma unroll 1
+      for (int kb = 0; kb < nfull; ++kb) block(kb, 32);
+      if (nfull < nblk) block(nfull, N - nfull * kT1Cols);
+
+      // ------------------------------------------------ per-pixel finish
+      // |h~'' - h''| <= delta: fp16 split (2^-21 relative per operand pair) plus
+      // the fp32 accumulation of 3J products; generous factor 2
+      const float delta = 2.0f * (4.7683716e-07f + 3 * J * 5.9604645e-08f) * bmax + 1e-30f;
+      const double band = c * fmax(kTieRtol, g.tau_amb) * (1.0 + fabs((double)m1 / c));
+      const float wnd = 2.0f * delta + (float)band * 1.001f + 1e-30f;
+      double u[J];
+      axis_table<D>(axis_coord(col, g.M), g.legendre != 0, u);
+      const double hG = eval_line<J>(coef_line + (int64_t)lab * J, u);
+      TcRare st;
+      st.m = CUDART_INF;
+      st.m2 = CUDART_INF;
+      st.cnt = 0;
+      st.flags = 0;
+      st.b0 = st.b1 = -1;
+      for (unsigned mk = mask1; mk; mk &= mk - 1u) {  // the candidate columns of block b1
+        const int i = b1 * kT1Cols + __ffs(mk) - 1;
+        tc_rare_update(st, i, eval_line<J>(coef_line + (int64_t)i * J, u), c);
+      }
+      bool found = st.cnt > 0 && !(st.flags & 2);
+      if (m2b <= m1 + wnd) {  // a second block is as close: exact min over both, re-scan
+        tc_exact_block<J>(st, coef_line, b2, N, u, c);
+        found = false;
+      } else {
+        st.m2 = fmin(st.m2, (double)m2b - (double)delta);  // out-of-block runner-up bound
+      }
+      const double refd = (double)ref;
+      const double aG = hG - refd;
+      const double eG = exp2(-aG);
+      const double sxd = (double)sx - (double)sxc;
+      const double sum = sxd + eG;
+      const double l2s = log2(sum);
+      const double l = (-aG - l2s) * 0.69314718055994530942;  // log p_G: objective.py:103-106
+      ell += l;
+      if (!isfinite(l) || !(bmax <= 3e38f)) nonfinite = 1;
+      if (g.tc_rec) {  // pass-2 record: p_i/2 * 2^13 = 2^(w13 + wl13 - h~''_i)
+        const double w13 = refd - 1.0 - l2s + 13.0;
+        const float wh = (float)w13;
+        float* rec = g.tc_rec + (line * (g.side / kTcPixTile) + (col >> 6)) * (4 * kTcPixTile) + (col & 63);
+        rec[0] = wh;
+        rec[kTcPixTile] = (float)(w13 - (double)wh);
+        rec[2 * kTcPixTile] = (float)(-4096.0 * sxd / sum);  // -(1 - p_G)/2 * 2^13
+        reinterpret_cast<int*>(rec)[3 * kTcPixTile] = lab;
+      }
+      const double m = st.cnt > 0 ? st.m : hG;
+      g.pix_m[p] = m / c;
+      e0 += (hG - m) / c;  // objective.py:119
+      if (!found) {
+        const int slot = atomicAdd(g.fix_count, 1);
+        g.fix_list[slot] = (int)p;
+      } else {
+        correct += (st.b0 == lab) ? 1 : 0;
+        amb += ((st.m2 - st.m) <= c * g.tau_amb * (1.0 + fabs(st.m / c))) ? 1 : 0;
+      }
     }
-    const bool found = st.cnt > 0 && !(st.flags & 2);
-    const double m = st.cnt > 0 ? st.m : hG;
-    g.pix_m[p] = m / c;
-    e0 += (hG - m) / c;  // objective.py:119
-    if (!found) {
-      const int slot = atomicAdd(g.fix_count, 1);
-      g.fix_list[slot] = (int)p;
-    } else {
-      correct += (st.b0 == lab[r]) ? 1 : 0;
-      amb += ((st.m2 - st.m) <= c * g.tau_amb * (1.0 + fabs(st.m / c))) ? 1 : 0;
+    // per-CTA partials: warp shuffle tree, then warps in fixed order
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      ell += __shfl_xor_sync(0xffffffffu, ell, off);
+      e0 += __shfl_xor_sync(0xffffffffu, e0, off);
+      correct += __shfl_xor_sync(0xffffffffu, correct, off);
+      amb += __shfl_xor_sync(0xffffffffu, amb, off);
+      nonfinite += __shfl_xor_sync(0xffffffffu, nonfinite, off);
+    }
+    if (lane == 0) {
+      red_d[warp][0] = ell;
+      red_d[warp][1] = e0;
+      red_i[warp][0] = correct;
+      red_i[warp][1] = amb;
+      red_i[warp][2] = nonfinite;
     }
   }
-  const double s_ell = block_sum<kTcThreads>(ell, red_d);
-  const double s_e0 = block_sum<kTcThreads>(e0, red_d);
-  const long long s_cor = block_sum<kTcThreads>(correct, red_i);
-  const long long s_amb = block_sum<kTcThreads>(amb, red_i);
-  const long long s_nf = block_sum<kTcThreads>(nonfinite, red_i);
+  tc_fence_before();
+  __syncthreads();
   if (tid == 0) {
+    double s_ell = 0.0, s_e0 = 0.0;
+    long long s_cor = 0, s_amb = 0, s_nf = 0;
+    for (int w = 0; w < kT1EpiWarps; ++w) {
+      s_ell += red_d[w][0];
+      s_e0 += red_d[w][1];
+      s_cor += red_i[w][0];
+      s_amb += red_i[w][1];
+      s_nf += red_i[w][2];
+    }
     g.part_d[2 * blockIdx.x + 0] = s_ell;
     g.part_d[2 * blockIdx.x + 1] = s_e0;
     g.part_i[4 * blockIdx.x + 0] = s_cor;
@@ -354,9 +448,7 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_tc_pass1(GridParams g) {
     g.part_i[4 * blockIdx.x + 2] = s_nf;
     g.part_i[4 * blockIdx.x + 3] = 0;
   }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, kTcTmemCols);
+  if (warp == kT1EpiWarps) tmem_dealloc(tmem, 512);
 }
 
 }  // namespace pgx

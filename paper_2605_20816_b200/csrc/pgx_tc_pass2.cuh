@@ -6,8 +6,12 @@
 //   epilogue     thread = grain = TMEM lane: r' = p/2 * 2^13 = 2^(w13 - h~''),
 //                or -(1 - p_G)/2 * 2^13 on the pixel's label grain; split into
 //                fp16 hi/lo and written BACK into TMEM over S (packed pairs)
-//   UMMA 2 (TS)  R[128 grains x 16] += [r'_hi r'_hi r'_lo]_tmem . [L_hi L_lo L_hi]^T
-//                (A operand from TMEM, K = 3 x 64 pixels, fp32 accumulate)
+//   UMMA 2 (TS)  R[128 grains x 32] += r'_hi . [L_hi | L_lo]^T + r'_lo . [L_hi | L_lo]^T
+//                (A operand from TMEM, K = 2 x 64 pixels, N = 32 = the hi and lo
+//                rows of L side by side; columns j and 16 + j are summed in the
+//                flush).  8 MMAs per tile: below N = 128 every tcgen05.mma costs
+//                a ~54-cycle floor (tools/umma_tput.cu), so the instruction count,
+//                not the flops, is what the tensor pipe spends here.
 //
 // Warp specialisation (FlashAttention-4 style), 288 threads, 2 CTAs per SM:
 //   warps 0-7  epilogue: warp w owns TMEM lanes 32 (w % 4) .. (grains) and the
@@ -22,7 +26,7 @@
 // group is flushed into fp64 line sums three tiles later (when it is known to
 // be complete) and per line expanded into the K gradient rows.
 //
-// TMEM (256 columns): S_0..S_2 [0, 192) (64 each), R_a [192, 208), R_b [208, 224).
+// TMEM (256 columns): S_0..S_2 [0, 192) (64 each), R_a [192, 224), R_b [224, 256).
 // Within S_s, pixel half h keeps r'_hi in [32h, 32h + 16) and r'_lo in
 // [32h + 16, 32h + 32): only columns its own warps have already read.
 #pragma once
@@ -54,30 +58,6 @@ struct TcP2Smem {
   static constexpr int TOTAL = REC_OFF + kTc2Buf * REC;
 };
 
-// registers written by an async TMEM load become usable after the wait; the
-// empty asm ties every use to it
-template <int N>
-__device__ __forceinline__ void tmem_regs_ready(uint32_t (&r)[N]) {
-#pragma unroll
-  for (int q = 0; q < N; ++q) asm volatile("" : "+r"(r[q]));
-}
-__device__ __forceinline__ void tmem_ld32_nowait(unsigned taddr, uint32_t (&s0)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(s0[0]), "=r"(s0[1]), "=r"(s0[2]), "=r"(s0[3]), "=r"(s0[4]), "=r"(s0[5]), "=r"(s0[6]),
-        "=r"(s0[7]), "=r"(s0[8]), "=r"(s0[9]), "=r"(s0[10]), "=r"(s0[11]), "=r"(s0[12]),
-        "=r"(s0[13]), "=r"(s0[14]), "=r"(s0[15]), "=r"(s0[16]), "=r"(s0[17]), "=r"(s0[18]),
-        "=r"(s0[19]), "=r"(s0[20]), "=r"(s0[21]), "=r"(s0[22]), "=r"(s0[23]), "=r"(s0[24]),
-        "=r"(s0[25]), "=r"(s0[26]), "=r"(s0[27]), "=r"(s0[28]), "=r"(s0[29]), "=r"(s0[30]),
-        "=r"(s0[31])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar))
-               : "memory");
-}
-
 // (line index, tile) walk over a CTA's items without divisions
 struct Tc2Cursor {
   int n = 0, li = 0, t = 0;
@@ -97,7 +77,7 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
   using L = TcP2Smem<J>;
   constexpr int KS = L::KS;
   constexpr uint32_t IDESC1 = umma_idesc_f16(128, kTc2Px);
-  constexpr uint32_t IDESC2 = umma_idesc_f16(128, 16);
+  constexpr uint32_t IDESC2 = umma_idesc_f16(128, 32);
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t bar_full[kTc2Buf], bar_a[2], bar_s[kTc2S], bar_p[kTc2S], bar_end;
   __shared__ unsigned tmem_base;
@@ -132,7 +112,7 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
     return c.t == ntiles - 1 || c.t % kTc2Group == kTc2Group - 1;
   };
   auto r_col = [&](const Tc2Cursor& c) {  // R accumulator of the item's group
-    return tmem + 192u + 16u * (unsigned)((c.li * gpl + c.t / kTc2Group) & 1);
+    return tmem + 192u + 32u * (unsigned)((c.li * gpl + c.t / kTc2Group) & 1);
   };
 
   if (warp == 8) {
@@ -186,19 +166,19 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
     while (cs.n < nitems && cs.n < kTc2S) issue_s();
     for (int k = 0; k < nitems; ++k) {
       const int st = k % kTc2S, b = k % kTc2Buf;
-      mbar_wait(&bar_p[st], (unsigned)(k / kTc2S) & 1u);  // r' of item k is in S_st
+      mbar_wait_sleep(&bar_p[st], (unsigned)(k / kTc2S) & 1u);  // r' of item k is in S_st
       tc_fence_after();
-      if (leader) {  // UMMA 2: R += [hi hi lo] . [L_hi L_lo L_hi]^T over the 64 pixels
+      if (leader) {  // UMMA 2: R += [r_hi; r_lo] . [L_hi | L_lo]^T over the 64 pixels
         const unsigned tr = r_col(cm);
         const unsigned ts = tmem + 64u * st;
         const uint64_t dl = d_pix + (uint64_t)((b * L::PIX + KS * (kTc2Px * 32)) >> 4);
         const bool fresh = cm.t % kTc2Group == 0;
 #pragma unroll
-        for (int s = 0; s < 3 * (kTc2Px / 16); ++s) {
+        for (int s = 0; s < 2 * (kTc2Px / 16); ++s) {
           const int p = s / (kTc2Px / 16), ks = s % (kTc2Px / 16);
-          // pixels [16 ks, 16 ks + 16): half ks / 2, packed columns 8 (ks % 2)
-          const unsigned a = ts + 32u * (ks >> 1) + 8u * (ks & 1) + (p == 2 ? 16u : 0u);
-          const uint64_t bo = dl + (uint64_t)(((p == 1 ? (kTc2Px / 16) * 512 : 0) + ks * 512) >> 4);
+          // pixels [16 ks, 16 ks + 16): half ks / 2, packed columns 8 (ks % 2); p = 1: r_lo
+          const unsigned a = ts + 32u * (ks >> 1) + 8u * (ks & 1) + (p == 1 ? 16u : 0u);
+          const uint64_t bo = dl + (uint64_t)((ks * 1024) >> 4);
           umma_f16_ts(tr, a, bo, IDESC2, !(fresh && s == 0));
         }
       }
@@ -211,7 +191,7 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
       if (k + 2 < nitems) {
         // UMMA 1 of item k + 2 complete => every MMA issued before it, incl. UMMA 2
         // of item k - 1: its buffer is free; so is a finished line's coefficient image
-        mbar_wait(&bar_s[(k + 2) % kTc2S], (unsigned)((k + 2) / kTc2S) & 1u);
+        mbar_wait_sleep(&bar_s[(k + 2) % kTc2S], (unsigned)((k + 2) / kTc2S) & 1u);
         if (cl.n < nitems) load_next();
         for (; cw.n <= k + 2; cw.advance(ntiles))  // every item up to k + 2 is done
           if (cw.t == ntiles - 1 && cw.li + 2 < nlines) load_coef(cw.li + 2);
@@ -229,12 +209,15 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
 #pragma unroll
     for (int j = 0; j < J; ++j) R64[j] = 0.0;
     auto flush = [&](const Tc2Cursor& c) {  // group of item c complete -> fp64; line -> K rows
-      uint32_t rv[16];
+      uint32_t rv[16], rw[16];
       tmem_ld16_nowait(r_col(c) + lane_off, rv);
+      tmem_ld16_nowait(r_col(c) + lane_off + 16u, rw);
       tmem_ld_wait();
       tmem_regs_ready(rv);
+      tmem_regs_ready(rw);
 #pragma unroll
-      for (int j = 0; j < J; ++j) R64[j] += (double)__uint_as_float(rv[j]);
+      for (int j = 0; j < J; ++j)
+        R64[j] += (double)__uint_as_float(rv[j]) + (double)__uint_as_float(rw[j]);
       if (c.t == ntiles - 1) {
         if (active) {
           const double* lcp = g.tc_lc + (l0 + c.li) * K;  // k_tc_coeffs

@@ -14,7 +14,7 @@
 
 using namespace pgx;
 
-__global__ void __launch_bounds__(128, 1) probe(int mode, int rounds, long long* out) {
+__global__ void __launch_bounds__(128, 1) probe(int mode, int rounds, long long* out, int pipelined) {
   __shared__ __align__(1024) unsigned char sm[128 * 32 * 4 + 64 * 32 * 2];
   __shared__ uint64_t mbar;
   __shared__ unsigned tbase;
@@ -55,9 +55,11 @@ __global__ void __launch_bounds__(128, 1) probe(int mode, int rounds, long long*
           umma_f16_ss(t + 128, umma_desc(sb + (s % 4) * 4096), umma_desc(sb + 16384 + (s % 4) * 512),
                       umma_idesc_f16(128, 16), s > 0);
       }
-      umma_commit(&mbar);
-      mbar_wait(&mbar, phase);
-      phase ^= 1u;
+      if (!pipelined || r == rounds + 3 || r == 3) {
+        umma_commit(&mbar);
+        mbar_wait(&mbar, phase);
+        phase ^= 1u;
+      }
       const long long c1 = clock64();
       if (r >= 4) total += c1 - c0;
     }
@@ -73,15 +75,16 @@ int main() {
   cudaMalloc(&d, 8 * sizeof(long long));
   const char* names[] = {"UMMA1 (2 x SS 128x64x16)", "UMMA2 (12 x TS 128x16x16)", "UMMA2 + UMMA1",
                          "UMMA2 as 4 x TS N32 + 4 x TS N16", "12 x SS 128x16x16"};
+  for (int pl = 0; pl < 2; ++pl)
   for (int m = 0; m < 5; ++m) {
-    probe<<<1, 128>>>(m, 200, d);
+    probe<<<1, 128>>>(m, 200, d, pl);
     if (cudaDeviceSynchronize() != cudaSuccess) {
       printf("error in mode %d\n", m);
       return 1;
     }
     long long v;
     cudaMemcpy(&v, d + m, sizeof(v), cudaMemcpyDeviceToHost);
-    printf("%-36s %6lld cycles\n", names[m], v);
+    printf("%-12s %-36s %6lld cycles\n", pl ? "throughput" : "latency", names[m], v);
   }
   return 0;
 }
