@@ -87,7 +87,6 @@ struct GridParams {
   double eps;
   double c;        // log2(e) / eps
   double tau_amb;
-  int dbg;         // experiment switches (PGX_DBG), 0 in production
   // outputs / scratch
   double* pix_m;   // min cost (h units) for the arg-min fix-up
   double* pix_w;   // w: p_i / 2 = 2^(w - h''_i) with w - h'' <= -1

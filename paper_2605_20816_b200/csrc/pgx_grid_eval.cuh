@@ -3,8 +3,6 @@
 // k_*.cu units do not implicitly instantiate each other's launchers).
 #pragma once
 
-#include <cstdlib>
-
 #include "pgx_grid.cuh"
 #include "pgx_launch.cuh"
 
@@ -54,10 +52,7 @@ inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool wa
   g.eps = e.eps;
   g.c = 1.4426950408889634074 / e.eps;
   g.tau_amb = e.tau_amb;
-  {
-    static const int dbg = getenv("PGX_DBG") ? atoi(getenv("PGX_DBG")) : 0;
-    g.dbg = dbg;
-  }
+
   g.pix_m = e.pix_m;
   g.pix_w = gp.pix_w;
   g.pix_q = gp.pix_q;

@@ -70,9 +70,20 @@ __device__ __forceinline__ void mbar_wait_addr(unsigned addr, unsigned parity) {
         : "r"(addr), "r"(parity)
         : "memory");
     if (done) return;
-    __nanosleep(32);
     if (spin == (1u << 30)) __trap();
   }
+}
+// non-blocking test of a phase
+__device__ __forceinline__ bool mbar_test_addr(unsigned addr, unsigned parity) {
+  unsigned done = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return done != 0;
 }
 __device__ __forceinline__ void mbar_arrive_addr(unsigned addr) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");

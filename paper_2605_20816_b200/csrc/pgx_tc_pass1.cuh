@@ -17,15 +17,16 @@
 // items are strided over the CTAs in a fixed order (deterministic partials).
 //
 // Epilogue, per 32-column block of one pixel (h~'' = S * inv):
-//   mb = block min (FMNMX3); the two best blocks (b1, b2) and their minima are
-//   tracked per pixel; the reference ref of s' = sum_{i != G} 2^(ref - h~''_i)
-//   moves only when the min falls more than kT1Stale below it (then s' is
-//   rescaled by 2^(ref_old - ref_new)): one FFMA + MUFU.EX2 + FADD per logit.
+//   mb = block min (FMNMX3); the three best block minima and, for the best
+//   two, the columns within 2 delta + tie band of their min (a bit mask) are
+//   tracked.  The reference ref of s' = sum_{i != G} 2^(ref - h~''_i) moves
+//   only when the min falls more than kT1Stale below it (s' is then rescaled
+//   by 2^(ref_old - ref_new)): one FFMA + MUFU.EX2 + FADD per logit.
 // Per pixel at the end: the label term in fp64, and the exact
-//   fp64 tie-tolerant arg-min / min / runner-up over the 32 grains of block b1
-//   — every logit within 2 delta + tie band of the fp32 min lies in b1 unless
-//   the runner-up block is that close too; such pixels (real cross-block ties)
-//   are queued for the exact re-scan of the tail kernel.
+//   fp64 tie-tolerant arg-min / min / runner-up over the masked columns of the
+//   best block (and of the second one when its min is that close).  A third
+//   block that close (real 3-way cross-block ties) queues the pixel for the
+//   exact re-scan of the tail kernel.
 #pragma once
 
 #include "pgx_grid_common.cuh"
@@ -96,22 +97,6 @@ struct TcP1Smem {
   static constexpr int RING = (200 * 1024 - IMG_OFF) / IMG < kT1Ring ? (200 * 1024 - IMG_OFF) / IMG : kT1Ring;
   static constexpr int TOTAL = IMG_OFF + RING * IMG;
 };
-
-// exact scan of one 32-grain block of a pixel (fixed order, tc_rare_update);
-// logits in groups of 8 so their coefficient loads are in flight together
-template <int J>
-__device__ __forceinline__ void tc_exact_block(TcRare& st, const double* coef_line, int blk, int N,
-                                               const double* u, double c) {
-  const int i0 = blk * 32, i1 = min(N, i0 + 32);
-  for (int ib = i0; ib < i1; ib += 8) {
-    double h[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) h[k] = ib + k < i1 ? eval_line<J>(coef_line + (int64_t)(ib + k) * J, u) : 0.0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (ib + k < i1) tc_rare_update(st, ib + k, h[k], c);
-  }
-}
 
 // named barrier of the 4 warps (128 threads) of one slot
 __device__ __forceinline__ void slot_sync(int s) {
@@ -273,9 +258,9 @@ __global__ void __launch_bounds__(kT1Threads, 1) k_tc_pass1(GridParams g) {
       const int lab = g.labels[p];
       const double* coef_line = g.tc_coef + line * (int64_t)N * J;
       const int2* meta = g.tc_meta + line * g.tc_nchunks;
-      float ref = CUDART_INF_F, m1 = CUDART_INF_F, m2b = CUDART_INF_F, bmax = 0.0f;
+      float ref = CUDART_INF_F, m1 = CUDART_INF_F, m2b = CUDART_INF_F, m3b = CUDART_INF_F, bmax = 0.0f;
       int b1 = 0, b2 = 0;
-      unsigned mask1 = 0u;          // columns of block b1 within the candidate window of its min
+      unsigned mask1 = 0u, mask2 = 0u;  // columns of blocks b1, b2 within the candidate window of their min
       float sx = 0.0f, sxc = 0.0f;  // Kahan-compensated sum of the block sums
       float inv = 0.0f, dblk = 0.0f;
       const double bandr = c * fmax(kTieRtol, g.tau_amb);
@@ -310,21 +295,28 @@ __global__ void __launch_bounds__(kT1Threads, 1) k_tc_pass1(GridParams g) {
         const float mb = fminf(fminf(fminf(t11[0], fminf(t11[1], t11[2])), fminf(t11[3], fminf(t11[4], t11[5]))),
                                fminf(fminf(t11[6], fminf(t11[7], t11[8])), fminf(t11[9], t11[10])));
         const float mbs = mb * inv;
-        if (mbs < m2b) {  // top-2 blocks (rare after the first few)
-          if (mbs < m1) {
-            // candidate columns of the new min block: within 2 delta + tie band of its min
+        if (mbs < m3b) {  // top-3 blocks (rare after the first few)
+          if (mbs < m2b) {
+            // candidate columns of the block: within 2 delta + tie band of its min
             const float thr = (mbs + 2.0f * dblk + (float)(bandr * (1.0 + fabs((double)mbs / c))) * 1.001f) / inv;
             unsigned mk = 0u;
 #pragma unroll
             for (int e = 0; e < 32; ++e) mk |= (w[e] <= thr) ? (1u << e) : 0u;
-            m2b = m1;
-            b2 = b1;
-            m1 = mbs;
-            b1 = kb;
-            mask1 = mk;
+            m3b = m2b;
+            if (mbs < m1) {
+              m2b = m1;
+              b2 = b1;
+              mask2 = mask1;
+              m1 = mbs;
+              b1 = kb;
+              mask1 = mk;
+            } else {
+              m2b = mbs;
+              b2 = kb;
+              mask2 = mk;
+            }
           } else {
-            m2b = mbs;
-            b2 = kb;
+            m3b = mbs;
           }
           if (mbs < ref - kT1Stale) {  // (also the first block: ref = +inf)
             const float nref = mbs - 1.0f;
@@ -372,17 +364,23 @@ __global__ void __launch_bounds__(kT1Threads, 1) k_tc_pass1(GridParams g) {
       st.cnt = 0;
       st.flags = 0;
       st.b0 = st.b1 = -1;
-      for (unsigned mk = mask1; mk; mk &= mk - 1u) {  // the candidate columns of block b1
-        const int i = b1 * kT1Cols + __ffs(mk) - 1;
+      // exact fp64 scan of the candidate columns: block b1, and block b2 when
+      // its min is as close (in index order: the tie rule picks the smallest)
+      const bool two = m2b <= m1 + wnd;
+      const int bl = two && b2 < b1 ? b2 : b1, bh = two && b2 < b1 ? b1 : b2;
+      const unsigned ml = two && b2 < b1 ? mask2 : mask1, mh = two && b2 < b1 ? mask1 : mask2;
+      for (unsigned mk = ml; mk; mk &= mk - 1u) {
+        const int i = bl * kT1Cols + __ffs(mk) - 1;
         tc_rare_update(st, i, eval_line<J>(coef_line + (int64_t)i * J, u), c);
       }
-      bool found = st.cnt > 0 && !(st.flags & 2);
-      if (m2b <= m1 + wnd) {  // a second block is as close: exact min over both, re-scan
-        tc_exact_block<J>(st, coef_line, b2, N, u, c);
-        found = false;
-      } else {
-        st.m2 = fmin(st.m2, (double)m2b - (double)delta);  // out-of-block runner-up bound
-      }
+      if (two)
+        for (unsigned mk = mh; mk; mk &= mk - 1u) {
+          const int i = bh * kT1Cols + __ffs(mk) - 1;
+          tc_rare_update(st, i, eval_line<J>(coef_line + (int64_t)i * J, u), c);
+        }
+      // a third block as close (or an overflowing candidate list): exact re-scan in the tail
+      bool found = st.cnt > 0 && !(st.flags & 2) && !(m3b <= m1 + wnd);
+      st.m2 = fmin(st.m2, (double)(two ? m3b : m2b) - (double)delta);  // out-of-block runner-up bound
       const double refd = (double)ref;
       const double aG = hG - refd;
       const double eG = exp2(-aG);

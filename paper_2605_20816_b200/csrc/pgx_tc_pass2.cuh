@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
     while (cs.n < nitems && cs.n < kTc2S) issue_s();
     for (int k = 0; k < nitems; ++k) {
       const int st = k % kTc2S, b = k % kTc2Buf;
-      mbar_wait_sleep(&bar_p[st], (unsigned)(k / kTc2S) & 1u);  // r' of item k is in S_st
+      mbar_wait(&bar_p[st], (unsigned)(k / kTc2S) & 1u);  // r' of item k is in S_st
       tc_fence_after();
       if (leader) {  // UMMA 2: R += [r_hi; r_lo] . [L_hi | L_lo]^T over the 64 pixels
         const unsigned tr = r_col(cm);
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
       if (k + 2 < nitems) {
         // UMMA 1 of item k + 2 complete => every MMA issued before it, incl. UMMA 2
         // of item k - 1: its buffer is free; so is a finished line's coefficient image
-        mbar_wait_sleep(&bar_s[(k + 2) % kTc2S], (unsigned)((k + 2) / kTc2S) & 1u);
+        mbar_wait(&bar_s[(k + 2) % kTc2S], (unsigned)((k + 2) / kTc2S) & 1u);
         if (cl.n < nitems) load_next();
         for (; cw.n <= k + 2; cw.advance(ntiles))  // every item up to k + 2 is done
           if (cw.t == ntiles - 1 && cw.li + 2 < nlines) load_coef(cw.li + 2);
