@@ -136,6 +136,48 @@ __device__ __forceinline__ T block_sum(T v, T* buf) {
   return r;
 }
 
+// Fixed-order block reduction of three fp64 and three integer partials with
+// one barrier: warp shuffle trees, then warp 0 folds the per-warp sums in
+// warp order (deterministic).  Result valid in thread 0.
+template <int kThreads>
+__device__ __forceinline__ void block_sum6(double& a, double& b, double& c, long long& x, long long& y,
+                                           long long& z) {
+  __shared__ double sd[kThreads / 32][3];
+  __shared__ long long si[kThreads / 32][3];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, off);
+    b += __shfl_xor_sync(0xffffffffu, b, off);
+    c += __shfl_xor_sync(0xffffffffu, c, off);
+    x += __shfl_xor_sync(0xffffffffu, x, off);
+    y += __shfl_xor_sync(0xffffffffu, y, off);
+    z += __shfl_xor_sync(0xffffffffu, z, off);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sd[w][0] = a;
+    sd[w][1] = b;
+    sd[w][2] = c;
+    si[w][0] = x;
+    si[w][1] = y;
+    si[w][2] = z;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a = b = c = 0.0;
+    x = y = z = 0;
+#pragma unroll
+    for (int v = 0; v < kThreads / 32; ++v) {
+      a += sd[v][0];
+      b += sd[v][1];
+      c += sd[v][2];
+      x += si[v][0];
+      y += si[v][1];
+      z += si[v][2];
+    }
+  }
+}
+
 // ---------------------------------------------------------------- pass 1
 template <int DIM, int D, bool EVAL>
 __global__ void __launch_bounds__(kP1Threads) k_general_pass1(EvalParams prm) {
@@ -348,8 +390,6 @@ struct StatsDev {
 };
 
 static __global__ void __launch_bounds__(256) k_finalize(FinalParams prm) {
-  __shared__ double rd[256];
-  __shared__ long long ri[256];
   const int tid = threadIdx.x;
   // fixed contiguous partition of the pass-1 partials per thread
   const int per = (prm.blocks1 + 255) / 256;
@@ -370,12 +410,7 @@ static __global__ void __launch_bounds__(256) k_finalize(FinalParams prm) {
     for (int64_t e = tid * per2; e < min(KN, (tid + 1) * per2); ++e)
       if (e % prm.N < prm.N - 1) th2 += prm.theta[e] * prm.theta[e];
   }
-  ell = block_sum<256>(ell, rd);
-  e0 = block_sum<256>(e0, rd);
-  th2 = block_sum<256>(th2, rd);
-  cor = block_sum<256>(cor, ri);
-  amb = block_sum<256>(amb, ri);
-  nf = block_sum<256>(nf, ri);
+  block_sum6<256>(ell, e0, th2, cor, amb, nf);
   if (tid == 0) {
     StatsDev* out = reinterpret_cast<StatsDev*>(prm.stats_out);
     const double P = (double)prm.P;
@@ -524,8 +559,6 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(EvalParams e, TailParams 
   if (!last) return;
   __threadfence();
   const FinalParams& prm = t.fin;
-  __shared__ double rd[kTailThreads];
-  __shared__ long long ri[kTailThreads];
   const int per = (prm.blocks1 + kTailThreads - 1) / kTailThreads;
   const int b0 = tid * per, b1 = min(prm.blocks1, b0 + per);
   double ell = 0.0, e0 = 0.0;
@@ -543,12 +576,7 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(EvalParams e, TailParams 
     const int per2 = (gridDim.x + kTailThreads - 1) / kTailThreads;
     for (int q = tid * per2; q < min((int)gridDim.x, (tid + 1) * per2); ++q) th2 += t.part_th2[q];
   }
-  ell = block_sum<kTailThreads>(ell, rd);
-  e0 = block_sum<kTailThreads>(e0, rd);
-  th2 = block_sum<kTailThreads>(th2, rd);
-  cor = block_sum<kTailThreads>(cor, ri);
-  amb = block_sum<kTailThreads>(amb, ri);
-  nf = block_sum<kTailThreads>(nf, ri);
+  block_sum6<kTailThreads>(ell, e0, th2, cor, amb, nf);
   if (tid == 0) {
     StatsDev* out = reinterpret_cast<StatsDev*>(prm.stats_out);
     const double P = (double)prm.P;
