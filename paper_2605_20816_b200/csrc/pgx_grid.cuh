@@ -75,12 +75,19 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
   for (int gt : {64, 32})
     if ((N + gt - 1) / gt * gt < (N + gp.GT - 1) / gp.GT * gp.GT) gp.GT = gt;
   gp.gtiles = (N + gp.GT - 1) / gp.GT;
-  const int target = 8 * sms;
-  gp.splits = std::max(1, std::min(gp.lines, (target + gp.gtiles - 1) / gp.gtiles));
+  const int K = feature_count(d->dim, d->degree);
+  // line splits: >= 8 CTAs per SM, up to 32 (small problems are latency
+  // bound: more, shorter CTAs fill the SMs) while the per-split gradient
+  // partials the tail reduces stay within 32 MB
+  {
+    const int s8 = std::max(1, std::min(gp.lines, (8 * sms + gp.gtiles - 1) / gp.gtiles));
+    const int s32 = std::max(1, std::min(gp.lines, (32 * sms + gp.gtiles - 1) / gp.gtiles));
+    const int cap = (int)std::max<int64_t>(1, (32LL << 20) / ((int64_t)K * N * 8));
+    gp.splits = std::max(s8, std::min(s32, cap));
+  }
   gp.lines_per_split = (gp.lines + gp.splits - 1) / gp.splits;
   gp.splits = (gp.lines + gp.lines_per_split - 1) / gp.lines_per_split;
   gp.splits_out = gp.splits;
-  const int K = feature_count(d->dim, d->degree);
   gp.smem2 = K * kG2Threads * 8;
   if (gp.tc && side % kTc2Px == 0) {
     // tensor-core pass 2: 128-grain tiles x line ranges, 2 CTAs per SM; the
