@@ -522,8 +522,18 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(EvalParams e, TailParams 
       for (int64_t ent = (int64_t)blockIdx.x * (kTailThreads / 32) + warp; ent < KN; ent += nw) {
         double a = 0.0;
         if (t.want_grad) {
-#pragma unroll 4
-          for (int s = lane; s < r.splits; s += 32) a += r.part_g[s * KN + ent];
+          // 8 loads in flight per lane (the partials are L2 reads one sector
+          // each), summed in split order
+          for (int s0 = lane; s0 < r.splits; s0 += 32 * 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int s = s0 + 32 * u;
+              v[u] = s < r.splits ? __ldcg(r.part_g + (int64_t)s * KN + ent) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a += v[u];
+          }
 #pragma unroll
           for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
         }
