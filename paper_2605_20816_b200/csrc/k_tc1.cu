@@ -6,8 +6,7 @@ namespace pgx {
 template <int DIM, int D>
 void tc_dispatch_pass1(const GridParams& g, int blocks, cudaStream_t s) {
   auto kern = k_tc_pass1<DIM, D>;
-  // padded so that one CTA (all 512 TMEM columns) occupies an SM
-  const int smem = std::max(TcP1Smem<D + 1>::TOTAL, kT1MinSmem);
+  const int smem = TcP1Smem<D + 1>::TOTAL;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -63,10 +63,10 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
   // 128 pixels share each chunk's coefficient build
   gp.tc = d->precision == PGX_PREC_TC;
   if (gp.tc) {
-    // tensor-core pass 1: persistent, one CTA per SM, items of kT1Slots tiles
+    // tensor-core pass 1: persistent, kT1CtasPerSm CTAs per SM, items of kT1Slots tiles
     const int64_t ntiles = (int64_t)gp.lines * (side / kTcThreadsTile);
     const int64_t items = (ntiles + kT1Slots - 1) / kT1Slots;
-    gp.tc_blocks = (int)std::min<int64_t>(items, sms);
+    gp.tc_blocks = (int)std::min<int64_t>(items, (int64_t)kT1CtasPerSm * sms);
     gp.blocks1 = gp.tc_blocks;
   }
   const int N = d->n_grains;

@@ -4,8 +4,8 @@
 // online log-sum-exp (objective.py:102-106) and the arg-min bookkeeping of
 // geometry.py:201-210.
 //
-// Persistent, warp-specialised, one CTA per SM (all 512 TMEM columns):
-//   warps 0-15  epilogue: slot s = warp / 4 is one tile of 128 pixels of a
+// Persistent, warp-specialised, kT1CtasPerSm CTAs per SM sharing TMEM:
+//   epilogue warps: slot s = warp / 4 is one tile of 128 pixels of a
 //               line, lane quarter warp % 4; thread = TMEM lane = pixel;
 //   warp 16     producer: bulk async copies of the per-line coefficient
 //               images (pgx_tc_coeffs.cuh) into a 3-stage ring, and one lane
@@ -36,14 +36,15 @@
 namespace pgx {
 
 constexpr int kTcThreadsTile = 128;              // pixels per tile (UMMA M, TMEM lanes)
-constexpr int kT1Slots = 4;                      // pixel tiles per item
+constexpr int kT1Slots = 2;                      // pixel tiles per item
+constexpr int kT1CtasPerSm = 2;                  // independent CTAs per SM (their sync phases interleave)
 constexpr int kT1EpiWarps = 4 * kT1Slots;        // 16
 constexpr int kT1Threads = 32 * kT1EpiWarps + 32;  // + producer warp
 constexpr int kT1Cols = 32;                      // grains per MMA (UMMA N) = one block
 constexpr int kT1Bufs = 4;                       // accumulator buffers per slot (TMEM)
 constexpr int kT1Ring = 16;                      // coefficient image ring (images in flight)
 constexpr float kT1Stale = 24.0f;                // ref may lag the min by this (log2 units)
-constexpr int kT1MinSmem = 120 * 1024;           // one CTA per SM (owns all of TMEM)
+constexpr int kT1SmemBudget = 100 * 1024;        // per CTA (kT1CtasPerSm share an SM)
 
 // exact per-pixel state for near-minimal logits
 struct TcRare {
@@ -94,7 +95,7 @@ struct TcP1Smem {
   static constexpr int IMG = tc_img_bytes<J>();
   static constexpr int A_OFF = 0;
   static constexpr int IMG_OFF = A_OFF + kT1Slots * A_SLOT;
-  static constexpr int RING = (200 * 1024 - IMG_OFF) / IMG < kT1Ring ? (200 * 1024 - IMG_OFF) / IMG : kT1Ring;
+  static constexpr int RING = (kT1SmemBudget - IMG_OFF) / IMG < kT1Ring ? (kT1SmemBudget - IMG_OFF) / IMG : kT1Ring;
   static constexpr int TOTAL = IMG_OFF + RING * IMG;
 };
 
@@ -104,7 +105,7 @@ __device__ __forceinline__ void slot_sync(int s) {
 }
 
 template <int DIM, int D>
-__global__ void __launch_bounds__(kT1Threads, 1) k_tc_pass1(GridParams g) {
+__global__ void __launch_bounds__(kT1Threads, kT1CtasPerSm) k_tc_pass1(GridParams g) {
   constexpr int J = D + 1;
   using L = TcP1Smem<J>;
   constexpr int KS = L::KS;
@@ -126,7 +127,8 @@ __global__ void __launch_bounds__(kT1Threads, 1) k_tc_pass1(GridParams g) {
   const int nimg = (N + kTcCoefChunk - 1) / kTcCoefChunk;
   const int nblk = (N + kT1Cols - 1) / kT1Cols;
 
-  if (warp == kT1EpiWarps) tmem_alloc(&tmem_base, 512);
+  constexpr unsigned kCols = kT1Slots * kT1Bufs * kT1Cols;  // TMEM columns of this CTA
+  if (warp == kT1EpiWarps) tmem_alloc(&tmem_base, kCols);
   if (tid == 32 * kT1EpiWarps) {
     for (int s = 0; s < kT1Slots; ++s)
       for (int b = 0; b < kT1Bufs; ++b) mbar_init(&bar_full[s][b], 1);
@@ -446,7 +448,7 @@ __global__ void __launch_bounds__(kT1Threads, 1) k_tc_pass1(GridParams g) {
     g.part_i[4 * blockIdx.x + 2] = s_nf;
     g.part_i[4 * blockIdx.x + 3] = 0;
   }
-  if (warp == kT1EpiWarps) tmem_dealloc(tmem, 512);
+  if (warp == kT1EpiWarps) tmem_dealloc(tmem, kCols);
 }
 
 }  // namespace pgx
