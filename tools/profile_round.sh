@@ -28,7 +28,7 @@ python3 - <<PY > $OUT/${TAG}_${CFG}_${PREC}_ncu_raw_key.txt
 import csv
 rows = list(csv.reader(open("/tmp/raw.csv")))
 hdr = rows[0]
-keys = [k for k in hdr if ("issue_stalled" in k and k.endswith("per_issue_active.ratio")) or any(s in k for s in ("Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_tensor_op", "sm__inst_executed_pipe_xu", "sm__pipe_fp64", "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak", "launch__registers_per_thread", "sm__throughput.avg.pct_of_peak"))]
+keys = [k for k in hdr if ("issue_stalled" in k and k.endswith("per_issue_active.ratio")) or any(s in k for s in ("Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_tensor_op", "sm__pipe_tensor_cycles_active.avg.pct", "sm__inst_executed_pipe_tmem", "sm__inst_executed_pipe_xu", "sm__pipe_fp64", "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak", "launch__registers_per_thread", "sm__throughput.avg.pct_of_peak"))]
 idx = [hdr.index(k) for k in keys]
 for r in rows[2:]:
     print(" | ".join(f"{hdr[i]}={r[i]}" for i in idx))
