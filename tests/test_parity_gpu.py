@@ -262,6 +262,28 @@ def test_fit_c1_trajectory(pgb):
     assert np.abs(got - ref).max() <= 1e-7 * (1 + np.abs(ref).max())
 
 
+@pytest.mark.parametrize("prec", ["exact", "tc"])
+def test_fit_device_loop_matches_host_loop(pgb, prec):
+    """fit(device_loop=True) keeps u, the gradient and the L-BFGS history on the
+    GPU; only dot-product summation order differs from the host loop."""
+    from paper_2605_20816_b200 import configs
+
+    z = gl.load("fit_traj")
+    w = configs.c1(labeler="host")
+    gm = pgb.GrainMap(grid=pgb.make_grid(64), labels=w.labels0 + 1, n_grains=20)
+    cfg = dict(degree=1, eps=0.05, max_iters=25, precision=prec)
+    host = pgb.fit(gm, pgb.FitConfig(**cfg))
+    dev = pgb.fit(gm, pgb.FitConfig(**cfg, device_loop=True))
+    a, b = np.asarray(host.phi_traj), np.asarray(dev.phi_traj)
+    assert a.shape == b.shape and dev.stop_reason == host.stop_reason
+    assert np.abs(a - b).max() <= 1e-9 * (1 + np.abs(a).max())
+    assert np.abs(dev.theta.values - host.theta.values).max() <= 1e-6 * (1 + np.abs(host.theta.values).max())
+    assert dev.gauge_residual == 0.0
+    if prec == "exact":
+        ref = np.asarray(z["c1_phi"])
+        assert np.abs(b - ref).max() <= 1e-7 * (1 + np.abs(ref).max())
+
+
 def test_errors_map_to_reference_exceptions(pgb):
     grid = pgb.make_grid(3)
     basis = pgb.DesignBasis.make("legendre", 1)
