@@ -130,6 +130,8 @@ class Problem:
         self._h = handle
         self._lock = threading.Lock()
         self._stats = _lib.PgxStats()
+        self._spec = (grid, basis_kind, degree, self._labels, int(device), stream, gdim)
+        self._exact = None
 
     # ------------------------------------------------------------------ basics
     @property
@@ -137,9 +139,30 @@ class Problem:
         return self._h
 
     def close(self):
+        if getattr(self, "_exact", None) is not None:
+            self._exact.close()
+            self._exact = None
         if getattr(self, "_h", None):
             self._lib.pgx_problem_destroy(self._h)
             self._h = None
+
+    # fp32 / fp16-split logits carry ~2^-22 relative error; beyond this bound
+    # on |h''| = |theta^T eta| / (eps ln 2) the error would reach 2^-6 in the
+    # exponent and the fast modes hand the call to the exact kernels
+    FAST_RANGE = 2.0 ** 16
+
+    def _fast_ok(self, t: np.ndarray, eps: float) -> bool:
+        if self.precision not in ("fp64", "tc"):
+            return True
+        bound = float(np.abs(t).sum(axis=0).max()) / (float(eps) * math.log(2.0))
+        return bound <= self.FAST_RANGE  # NaN/inf: False -> the exact path reports them
+
+    def _exact_problem(self) -> "Problem":
+        if self._exact is None:
+            grid, kind, degree, labels, device, stream, dim = self._spec
+            self._exact = Problem(grid, kind, degree, self.n_grains, labels, precision="exact",
+                                  device=device, stream=stream, dim=dim)
+        return self._exact
 
     def __del__(self):
         try:
@@ -178,6 +201,9 @@ class Problem:
              want_assign: bool = False) -> tuple[EvalResult, EvalStats]:
         """One fused evaluation with host buffers (copies inside the call)."""
         t, tflag = self._theta(theta)
+        if not self._fast_ok(t, eps):
+            return self._exact_problem().eval(theta, eps, lam=lam, want_grad=want_grad,
+                                              want_assign=want_assign)
         flags = tflag | (_lib.PGX_WANT_GRAD if want_grad else 0) | (
             _lib.PGX_WANT_ASSIGN if want_assign else 0)
         grad = np.empty((self.K, self.n_grains)) if want_grad else None
@@ -201,6 +227,8 @@ class Problem:
     def assign(self, theta, *, with_margin: bool = False):
         """Tie-tolerant hard assignment (1-based labels) without the N x P costs."""
         t, tflag = self._theta(theta)
+        if not self._fast_ok(t, 1.0):  # (the arg-min does not depend on eps)
+            return self._exact_problem().assign(theta, with_margin=with_margin)
         labels = np.empty(self.n_points, dtype=np.int64)
         margin = np.empty(self.n_points, dtype=np.float32) if with_margin else None
         with self._lock:

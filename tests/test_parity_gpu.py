@@ -335,3 +335,48 @@ def test_drop_in_with_reference_style_objects(pgb):
     assert phi == pytest.approx(float(z["phi1"]), rel=FP64_PHI)
     g = pgb.gradient(T(th), D(), GM(), 0.5)
     assert np.abs(g - z["grad1"]).max() <= 1e-6 * np.abs(z["grad1"]).max()
+
+
+EDGE = {
+    # name: (degree, n_grains, theta scale, eps, label rule)
+    "theta_1e8": (2, 12, 1e8, 0.05, "random"),      # no overflow (test_objective.py:52-57)
+    "two_grains": (2, 2, 1.0, 0.02, "random"),      # N = 2, the smallest allowed (geometry.py:94-95)
+    "one_label": (2, 9, 1.0, 0.02, "single"),       # every pixel in one grain, the rest empty
+    "degree0": (0, 33, 1.0, 0.05, "random"),        # K = 1: constant costs, ties everywhere
+    "tiny_eps": (3, 40, 1.0, 1e-4, "argmin"),       # |h|/eps ~ 1e4: one dominant grain per pixel
+    "n_not_x32": (2, 45, 0.3, 0.02, "argmin"),      # partial 32-grain block
+}
+
+
+@pytest.mark.parametrize("prec", ["fp64", "tc"])
+@pytest.mark.parametrize("case", sorted(EDGE))
+def test_edge_cases_regular_grid(pgb, case, prec):
+    """The grid/tensor-core paths against the fp64 oracle on edge inputs of a
+    128 x 128 grid (the smallest side the separable paths take)."""
+    d, n, scale, eps, rule = EDGE[case]
+    rng = np.random.default_rng(7)
+    m = 64
+    pts = oracle.grid_points(m)
+    k = (d + 1) * (d + 2) // 2
+    theta = rng.normal(size=(k, n)) * scale
+    if rule == "random":
+        labels0 = rng.integers(0, n, len(pts))
+    elif rule == "single":
+        labels0 = np.full(len(pts), 3, dtype=np.int64)
+    else:
+        labels0 = oracle.hard_assign_points(theta, "legendre", d, pts) - 1
+        flip = rng.random(len(pts)) < 0.05
+        labels0[flip] = rng.integers(0, n, int(flip.sum()))
+    ref = oracle.evaluate_problem(theta, "legendre", d, pts, labels0, eps, want_grad=True,
+                                  want_assign=True)
+    prob = pgb.Problem(pgb.make_grid(m), "legendre", d, n, labels0, precision=prec)
+    res, st = prob.eval(theta, eps, want_grad=True, want_assign=True)
+    tp, tg = TOL[prec]
+    assert np.isfinite(res.phi) and np.all(np.isfinite(res.grad))
+    assert abs(res.phi - ref.phi) <= tp * (1 + abs(ref.phi)), (res.phi, ref.phi)
+    assert np.abs(res.grad - ref.grad).max() <= tg * max(np.abs(ref.grad).max(), 1e-300)
+    assert abs(res.err - ref.err) <= st.n_ambiguous / len(pts) + 1e-15
+    assert abs(res.e0 - ref.e0) <= tp * (1 + abs(ref.e0))
+    labels = prob.assign(theta)
+    assert np.array_equal(labels, oracle.hard_assign_points(theta, "legendre", d, pts))
+    prob.close()
