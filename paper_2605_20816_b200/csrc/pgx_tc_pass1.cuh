@@ -265,12 +265,16 @@ __global__ void __launch_bounds__(kT1Threads, kT1CtasPerSm) k_tc_pass1(GridParam
       unsigned mask1 = 0u, mask2 = 0u;  // columns of blocks b1, b2 within the candidate window of their min
       float sx = 0.0f, sxc = 0.0f;  // Kahan-compensated sum of the block sums
       float inv = 0.0f, dblk = 0.0f;
-      const double bandr = c * fmax(kTieRtol, g.tau_amb);
+      // candidate window terms in fp32 (a window, widened by 0.1%): no fp64
+      // division on the per-block path
+      const float bandf = (float)(c * fmax(kTieRtol, g.tau_amb)), inv_cf = (float)(1.0 / c);
+      float rinv = 0.0f;  // 1 / inv (exact: powers of two)
       // one 32-grain block: wait, load, refill, min bookkeeping, exponentials
       auto block = [&](int kb, int cn) {
         const unsigned buf = (unsigned)(rc % kT1Bufs);
         if (kb % QB == 0) {
           const int2 mt = __ldg(meta + kb / QB);
+          rinv = __int_as_float((127 + (mt.x + 10)) << 23);
           inv = __int_as_float((127 - (mt.x + 10)) << 23);  // 2^-(sB + 10): S * inv = h~''
           const float bn = __int_as_float(mt.y);
           bmax = fmaxf(bmax, bn);
@@ -300,7 +304,7 @@ __global__ void __launch_bounds__(kT1Threads, kT1CtasPerSm) k_tc_pass1(GridParam
         if (mbs < m3b) {  // top-3 blocks (rare after the first few)
           if (mbs < m2b) {
             // candidate columns of the block: within 2 delta + tie band of its min
-            const float thr = (mbs + 2.0f * dblk + (float)(bandr * (1.0 + fabs((double)mbs / c))) * 1.001f) / inv;
+            const float thr = (mbs + 2.0f * dblk + bandf * (1.0f + fabsf(mbs) * inv_cf) * 1.001f) * rinv;
             unsigned mk = 0u;
 #pragma unroll
             for (int e = 0; e < 32; ++e) mk |= (w[e] <= thr) ? (1u << e) : 0u;
