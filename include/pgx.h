@@ -138,6 +138,16 @@ pgx_status pgx_eval(pgx_problem* problem, const void* theta, double eps, double 
 pgx_status pgx_assign(pgx_problem* problem, const void* theta, uint32_t flags,
                       int64_t* labels_out, float* margin_out, pgx_stats* stats_out);
 
+/* Per-grain label moments of a regular 2-D grid (make_grid(resolution)), the
+ * input of the moment heuristic (heuristics.py:46-73, np.bincount of 1, x_a and
+ * x_a x_b by label).  out[6 i + q], q = 0..5, receives the exact integer sums of
+ * {1, a1, a2, a1^2, a1 a2, a2^2} over the pixels of grain i, where
+ * a = 2 resolution x is the odd integer coordinate.  labels0: host, 0-based.
+ * Stand-alone (no problem handle); synchronous. */
+pgx_status pgx_label_moments(int resolution, int64_t n_points, const int64_t* labels0, int n_grains,
+                             int64_t* out);
+const char* pgx_label_moments_error(void);
+
 /* Number of kernel launches the last pgx_eval / pgx_assign enqueued. */
 int pgx_last_launch_count(pgx_problem* problem);
 

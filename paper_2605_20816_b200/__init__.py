@@ -33,6 +33,7 @@ from .objective import (
     hard_assign,
     objective,
 )
+from .heuristics import MomentSummary, heuristic_theta, moments
 from .optimizer import FitConfig, FitReport, fit, init_zero, line_search
 
 __version__ = "0.1.0"
@@ -44,5 +45,5 @@ __all__ = [
     "ResourceError", "TIE_RTOL", "GrainMap", "PixelGrid", "accuracy_and_error", "make_grid",
     "EvalResult", "EvalStats", "Problem", "energy_eps", "energy_zero", "evaluate_objective",
     "gradient", "hard_assign", "objective", "FitConfig", "FitReport", "fit", "init_zero",
-    "line_search",
+    "line_search", "MomentSummary", "heuristic_theta", "moments",
 ]

@@ -86,6 +86,8 @@ SIGNATURES = {
     "pgx_profile_name": (c_char_p, [c_void_p, c_int]),
     "pgx_profile_ms": (c_float, [c_void_p, c_int]),
     "pgx_synchronize": (c_int, [c_void_p]),
+    "pgx_label_moments": (c_int, [c_int, ctypes.c_int64, c_void_p, c_int, c_void_p]),
+    "pgx_label_moments_error": (c_char_p, []),
 }
 
 _lib = None
