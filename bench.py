@@ -353,9 +353,11 @@ def run_ours(args):
         v["frac"] = v["achieved"] / v["peak"]
     binding = max(("fp64", "mufu_ex2") if args.precision != "tc" else ("tensor", "mufu_ex2"),
                   key=lambda k: pipes[k]["frac"])
+    traffic, traffic_src = measured_traffic(args.config, args.precision, top)
     roofline = {
         "bound": "tensor", "achieved": pipes["tensor"]["achieved"], "peak": pipes["tensor"]["peak"],
-        "unit": "TFLOP/s", "frac": pipes["tensor"]["frac"], "traffic": None,
+        "unit": "TFLOP/s", "frac": pipes["tensor"]["frac"], "traffic": traffic,
+        "traffic_source": traffic_src, "algorithmic_bytes": bytes_top,
         "kernel": top, "kernel_ms": avg[top], "kernel_share": avg[top] / (sum(avg.values())),
         "peak_kind": f"{peaks_kind} (bf16 burst, MEASURED_PEAKS.json)",
         "binding_pipe": binding, "binding_frac": pipes[binding]["frac"], "pipes": pipes,
@@ -402,6 +404,23 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def measured_traffic(config: str, precision: str, kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the latest committed
+    ncu --set full capture (profiles/*_traffic.json, written from the .ncu-rep
+    of tools/profile_round.sh), or (None, None)."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                              "profiles", "*_traffic.json")), reverse=True):
+        try:
+            with open(path) as f:
+                ent = json.load(f).get(f"{config}_{precision}:{kernel}")
+        except (OSError, ValueError):
+            continue
+        if ent:
+            return ent["dram_bytes_read"] + ent["dram_bytes_write"], os.path.relpath(path)
+    return None, None
 
 
 # arithmetic the path computes in, per precision mode

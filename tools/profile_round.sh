@@ -36,3 +36,23 @@ PY
 for k in pass1 pass2; do python3 tools/sass_hot.py /tmp/prof_${TAG}_${CFG}_${PREC}.ncu-rep $k 30 > $OUT/${TAG}_${CFG}_${PREC}_sass_$k.txt 2>&1; done
 cp /tmp/prof_${TAG}_${CFG}_${PREC}.ncu-rep $OUT/ 2>/dev/null
 ls $OUT
+# DRAM bytes per launch per kernel (bench.py reads the latest profiles/*_traffic.json)
+python3 - "$OUT" "$TAG" "$CFG" "$PREC" <<'PY'
+import csv, io, json, subprocess, sys
+out_dir, tag, cfg, prec = sys.argv[1:5]
+raw = subprocess.run(["ncu", "-i", f"/tmp/prof_{tag}_{cfg}_{prec}.ncu-rep", "--page", "raw", "--csv"],
+                     capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+res = {}
+if len(rows) > 2:
+    h, units = rows[0], rows[1]
+    for r in rows[2:]:
+        d, u = dict(zip(h, r)), dict(zip(h, units))
+        kern = d["Kernel Name"].split("<")[0].replace("void ", "").replace("pgx::", "").replace("k_", "", 1)
+        res[f"{cfg}_{prec}:{kern}"] = {
+            "dram_bytes_read": float(d["dram__bytes_read.sum"]) * scale[u["dram__bytes_read.sum"]],
+            "dram_bytes_write": float(d["dram__bytes_write.sum"]) * scale[u["dram__bytes_write.sum"]],
+            "kernel": d["Kernel Name"], "duration": d["gpu__time_duration.sum"] + " " + u["gpu__time_duration.sum"]}
+json.dump(res, open(f"{out_dir}/{tag}_{cfg}_{prec}_traffic.json", "w"), indent=1, sort_keys=True)
+PY
