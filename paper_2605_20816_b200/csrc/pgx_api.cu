@@ -108,6 +108,7 @@ struct pgx_problem {
                     d_labels_out, d_margin_out, grid.d_part, grid.d_tc, grid.d_tc_pix};
     for (void* b : bufs)
       if (b) cudaFree(b);
+    grid_plan_destroy(grid);
     for (cudaEvent_t& e : prof_ev)
       if (e) cudaEventDestroy(e);
   }

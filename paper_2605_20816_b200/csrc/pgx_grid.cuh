@@ -4,6 +4,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "pgx_grid_common.cuh"
 #include "pgx_grid_pass1.cuh"
@@ -38,7 +39,40 @@ struct GridPlan {
   double* pix_w = nullptr;
   float* pix_q = nullptr;
   int smem2 = 0;
+  // tc: the evaluation in line chunks so that pass 2 of chunk c (stream aux)
+  // runs while pass 1 of chunk c + 1 (the problem's stream) does: one CTA of
+  // each kernel per SM, whose latency-bound phases interleave
+  static constexpr int kMaxChunks = 8;
+  int tc_chunks = 1;
+  int64_t ch_tile[kMaxChunks + 1] = {};  // pass-1 tile range of chunk c: [ch_tile[c], ch_tile[c+1])
+  int ch_p1grid[kMaxChunks] = {};
+  int ch_part[kMaxChunks + 1] = {};      // pass-1 partial slots
+  int64_t ch_line[kMaxChunks + 1] = {};  // pass-2 line range
+  int ch_lps[kMaxChunks] = {}, ch_splits[kMaxChunks] = {};
+  int ch_split[kMaxChunks + 1] = {};     // pass-2 split slots
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_p1[kMaxChunks] = {};
+  cudaEvent_t ev_join = nullptr;
 };
+
+// pass-2 line splits over `lines` lines: minimise waves x (lines per CTA + 1)
+inline void tc2_splits_for(int lines, int gtiles, int64_t slots, int cap, int& lps_out, int& splits_out) {
+  int64_t best = -1;
+  lps_out = lines;
+  splits_out = 1;
+  for (int sp = 1; sp <= std::min(lines, cap); ++sp) {
+    const int lps = (lines + sp - 1) / sp;
+    const int spr = (lines + lps - 1) / lps;
+    if (spr != sp) continue;
+    const int64_t waves = ((int64_t)gtiles * spr + slots - 1) / slots;
+    const int64_t cost = waves * (lps + 1);  // + ~1 line of per-CTA pipeline fill
+    if (best < 0 || cost < best) {
+      best = cost;
+      lps_out = lps;
+      splits_out = spr;
+    }
+  }
+}
 
 inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
   gp.enabled = false;
@@ -94,22 +128,35 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
     // split count minimises waves x lines-per-CTA (ties: fewer splits, so the
     // tail reduces less)
     gp.tc2_gtiles = (N + kTc2Grains - 1) / kTc2Grains;
-    const int64_t slots = 2LL * sms;
-    int64_t best = -1;
-    for (int sp = 1; sp <= std::min(gp.lines, 8 * sms); ++sp) {
-      const int lps = (gp.lines + sp - 1) / sp;
-      const int spr = (gp.lines + lps - 1) / lps;
-      if (spr != sp) continue;
-      const int64_t waves = ((int64_t)gp.tc2_gtiles * spr + slots - 1) / slots;
-      const int64_t cost = waves * (lps + 1);  // + ~1 line of per-CTA pipeline fill
-      if (best < 0 || cost < best) {
-        best = cost;
-        gp.tc2_lps = lps;
-        gp.tc2_splits = spr;
-      }
-    }
+    tc2_splits_for(gp.lines, gp.tc2_gtiles, 2LL * sms, 8 * sms, gp.tc2_lps, gp.tc2_splits);
     gp.splits_out = gp.tc2_splits;
-    gp.part_splits = std::max(gp.splits, gp.tc2_splits);
+    // line chunks (>= 64 lines each): pass 1 one CTA per SM, pass 2 sized for
+    // the other half of each SM
+    const int tpl = side / kTcThreadsTile;
+    // (measured: c5 4 chunks 20.1 ms vs 17.3 ms unchunked -- each kernel at one
+    // CTA per SM loses more than the interleaving gains; off unless requested)
+    const char* env = getenv("PGX_TC_CHUNKS");
+    int C = env ? atoi(env) : 1;
+    C = std::max(1, std::min({C, GridPlan::kMaxChunks, gp.lines / 64}));
+    gp.tc_chunks = C;
+    if (C > 1) {
+      gp.ch_part[0] = 0;
+      gp.ch_split[0] = 0;
+      for (int c = 0; c <= C; ++c) gp.ch_line[c] = (int64_t)gp.lines * c / C;
+      for (int c = 0; c < C; ++c) {
+        const int nl = (int)(gp.ch_line[c + 1] - gp.ch_line[c]);
+        gp.ch_tile[c] = gp.ch_line[c] * tpl;
+        const int64_t items = ((int64_t)nl * tpl + kT1Slots - 1) / kT1Slots;
+        gp.ch_p1grid[c] = (int)std::min<int64_t>(items, sms);
+        gp.ch_part[c + 1] = gp.ch_part[c] + gp.ch_p1grid[c];
+        tc2_splits_for(nl, gp.tc2_gtiles, (int64_t)sms, 8 * sms, gp.ch_lps[c], gp.ch_splits[c]);
+        gp.ch_split[c + 1] = gp.ch_split[c] + gp.ch_splits[c];
+      }
+      gp.ch_tile[C] = (int64_t)gp.lines * tpl;
+      gp.blocks1 = gp.ch_part[C];
+      gp.splits_out = gp.ch_split[C];
+    }
+    gp.part_splits = std::max(gp.splits, gp.splits_out);
   }
 }
 
@@ -158,8 +205,22 @@ inline cudaError_t grid_plan_create(GridPlan& gp, const pgx_desc* d, int sms, si
       gp.tc_pix = static_cast<unsigned char*>(gp.d_tc_pix);
       gp.tc_pix_ready = false;
     }
+    if (gp.tc_chunks > 1) {
+      e = cudaStreamCreateWithFlags(&gp.aux, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return e;
+      for (int c = 0; c < gp.tc_chunks; ++c)
+        if ((e = cudaEventCreateWithFlags(&gp.ev_p1[c], cudaEventDisableTiming)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&gp.ev_join, cudaEventDisableTiming)) != cudaSuccess) return e;
+    }
   }
   return cudaSuccess;
+}
+
+inline void grid_plan_destroy(GridPlan& gp) {
+  for (cudaEvent_t& ev : gp.ev_p1)
+    if (ev) cudaEventDestroy(ev), ev = nullptr;
+  if (gp.ev_join) cudaEventDestroy(gp.ev_join), gp.ev_join = nullptr;
+  if (gp.aux) cudaStreamDestroy(gp.aux), gp.aux = nullptr;
 }
 
 }  // namespace pgx

@@ -107,6 +107,12 @@ struct GridParams {
   int tc_nchunks;
   double* tc_lc;                // [lines][K] line factors (k_tc_coeffs)
   const unsigned char* tc_pix;  // [side / 64] pass-2 pixel operand tiles (k_tc_pix)
+  // tensor-core launches over a part of the evaluation (line chunks that
+  // overlap pass 1 of one chunk with pass 2 of the previous one)
+  int64_t tile_lo, tile_hi;     // pass 1: tiles [tile_lo, tile_hi) of 128 pixels
+  int part_off;                 // pass 1: first per-CTA partial slot
+  int64_t line_lo;              // pass 2: first line (g.lines = end line)
+  int split_off;                // pass 2: first gradient-partial split slot
   float* tc_rec;                // [lines][side / 64][4][64] pass-2 pixel records
                                 // (w13, wl13, qn, label) written by TC pass 1
 };

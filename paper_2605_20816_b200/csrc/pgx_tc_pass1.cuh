@@ -122,8 +122,9 @@ __global__ void __launch_bounds__(kT1Threads, kT1CtasPerSm) k_tc_pass1(GridParam
   const int N = g.N;
   const double c = g.c;
   const int tpl = g.side / kTcThreadsTile;  // tiles per line
-  const int64_t ntiles = (int64_t)g.lines * tpl;
-  const int64_t nitems = (ntiles + kT1Slots - 1) / kT1Slots;
+  // this launch's tiles [tbase, ntiles) (a line range of the evaluation)
+  const int64_t tbase = g.tile_lo, ntiles = g.tile_hi;
+  const int64_t nitems = (ntiles - tbase + kT1Slots - 1) / kT1Slots;
   const int nimg = (N + kTcCoefChunk - 1) / kTcCoefChunk;
   const int nblk = (N + kT1Cols - 1) / kT1Cols;
 
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(kT1Threads, kT1CtasPerSm) k_tc_pass1(GridParam
   // the images of a chunk: one per distinct line among the item's tiles;
   // js[s] = index of slot s's image, returns the count
   auto distinct = [&](int64_t it, int (&js)[kT1Slots]) {
-    const int64_t t0 = it * kT1Slots;
+    const int64_t t0 = tbase + it * kT1Slots;
     int n = 0;
     for (int s = 0; s < kT1Slots; ++s) {
       if (s > 0 && t0 + s < ntiles && (t0 + s) / tpl == (t0 + s - 1) / tpl)
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(kT1Threads, kT1CtasPerSm) k_tc_pass1(GridParam
           if (leader) {
             int s = 0;
             while (js[s] != j) ++s;  // first tile slot of distinct line j
-            const int64_t line = (it * kT1Slots + s) / tpl;
+            const int64_t line = (tbase + it * kT1Slots + s) / tpl;
             mbar_arrive_expect_tx(&bar_img[slot], L::IMG);
             bulk_g2s(smem + L::IMG_OFF + slot * L::IMG,
                      g.tc_img + (line * g.tc_nchunks + ci) * (int64_t)L::IMG, L::IMG, &bar_img[slot]);
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(kT1Threads, kT1CtasPerSm) k_tc_pass1(GridParam
     for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
       int js[kT1Slots];
       const int nl = distinct(it, js);
-      const int64_t tile = it * kT1Slots + s;
+      const int64_t tile = tbase + it * kT1Slots + s;
       const bool active = tile < ntiles;
       const int64_t line = active ? tile / tpl : 0;
       const int col = (int)(tile % tpl) * kTcThreadsTile + prow;
@@ -445,12 +446,13 @@ __global__ void __launch_bounds__(kT1Threads, kT1CtasPerSm) k_tc_pass1(GridParam
       s_amb += red_i[w][1];
       s_nf += red_i[w][2];
     }
-    g.part_d[2 * blockIdx.x + 0] = s_ell;
-    g.part_d[2 * blockIdx.x + 1] = s_e0;
-    g.part_i[4 * blockIdx.x + 0] = s_cor;
-    g.part_i[4 * blockIdx.x + 1] = s_amb;
-    g.part_i[4 * blockIdx.x + 2] = s_nf;
-    g.part_i[4 * blockIdx.x + 3] = 0;
+    const int64_t b = g.part_off + blockIdx.x;  // partial slot of this CTA
+    g.part_d[2 * b + 0] = s_ell;
+    g.part_d[2 * b + 1] = s_e0;
+    g.part_i[4 * b + 0] = s_cor;
+    g.part_i[4 * b + 1] = s_amb;
+    g.part_i[4 * b + 2] = s_nf;
+    g.part_i[4 * b + 3] = 0;
   }
   if (warp == kT1EpiWarps) tmem_dealloc(tmem, kCols);
 }

@@ -84,7 +84,8 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gbase = blockIdx.x * kTc2Grains;
-  const int64_t l0 = (int64_t)blockIdx.y * g.lines_per_split;
+  // lines [line_lo, lines) of this launch, lines_per_split per CTA row
+  const int64_t l0 = g.line_lo + (int64_t)blockIdx.y * g.lines_per_split;
   const int nlines = (int)(min((int64_t)g.lines, l0 + g.lines_per_split) - l0);
   const int ntiles = g.side / kTc2Px;
   const int gpl = (ntiles + kTc2Group - 1) / kTc2Group;  // R groups per line
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
     const int i = gbase + 32 * q + lane;     // this thread's grain (TMEM lane)
     const bool active = i < g.N;
     const unsigned lane_off = (unsigned)(32 * q) << 16;
-    double* acc = g.part_g + (int64_t)blockIdx.y * K * g.N + (active ? i : 0);
+    double* acc = g.part_g + (int64_t)(g.split_off + blockIdx.y) * K * g.N + (active ? i : 0);
     const double rs = -2.0 / (8192.0 * 1024.0);  // R_true = -2 acc 2^-(13 + 10): r' = -r
     double R64[J];
 #pragma unroll

@@ -382,3 +382,24 @@ def test_edge_cases_regular_grid(pgb, case, prec):
     labels = prob.assign(theta)
     assert np.array_equal(labels, oracle.hard_assign_points(theta, "legendre", d, pts))
     prob.close()
+
+
+def test_tc_line_chunks_match_single_launch(pgb, monkeypatch):
+    """PGX_TC_CHUNKS=k splits a tc evaluation into k line chunks whose pass 2
+    overlaps the next chunk's pass 1 on a second stream: same results up to the
+    order of the partial sums."""
+    from paper_2605_20816_b200 import configs
+
+    w = configs.make("c2", labeler="gpu")
+    th = np.asarray(w.theta_bench, dtype=np.float64)
+    base = pgb.Problem(w.grid, w.kind, w.degree, w.n_grains, w.labels0, precision="tc")
+    a, sa = base.eval(th, w.eps, lam=w.lam, want_assign=True)
+    monkeypatch.setenv("PGX_TC_CHUNKS", "4")
+    ch = pgb.Problem(w.grid, w.kind, w.degree, w.n_grains, w.labels0, precision="tc")
+    b, sb = ch.eval(th, w.eps, lam=w.lam, want_assign=True)
+    assert abs(a.phi - b.phi) <= 1e-12 * (1 + abs(a.phi))
+    assert np.abs(a.grad - b.grad).max() <= 1e-10 * np.abs(a.grad).max()
+    assert a.err == b.err and sa.n_ambiguous == sb.n_ambiguous
+    assert a.e0 == pytest.approx(b.e0, rel=1e-12)
+    base.close()
+    ch.close()
