@@ -271,16 +271,16 @@ __global__ void __launch_bounds__(kT1Threads, kT1CtasPerSm) k_tc_pass1(GridParam
       const float bandf = (float)(c * fmax(kTieRtol, g.tau_amb)), inv_cf = (float)(1.0 / c);
       float rinv = 0.0f;  // 1 / inv (exact: powers of two)
       // one 32-grain block: wait, load, refill, min bookkeeping, exponentials
+      auto chunk_meta = [&](int ci) {  // scale and error bound of 128-grain chunk ci
+        const int2 mt = __ldg(meta + ci);
+        rinv = __int_as_float((127 + (mt.x + 10)) << 23);
+        inv = __int_as_float((127 - (mt.x + 10)) << 23);  // 2^-(sB + 10): S * inv = h~''
+        const float bn = __int_as_float(mt.y);
+        bmax = fmaxf(bmax, bn);
+        dblk = 2.0f * (4.7683716e-07f + 3 * J * 5.9604645e-08f) * bn + 1e-30f;
+      };
       auto block = [&](int kb, int cn) {
         const unsigned buf = (unsigned)(rc % kT1Bufs);
-        if (kb % QB == 0) {
-          const int2 mt = __ldg(meta + kb / QB);
-          rinv = __int_as_float((127 + (mt.x + 10)) << 23);
-          inv = __int_as_float((127 - (mt.x + 10)) << 23);  // 2^-(sB + 10): S * inv = h~''
-          const float bn = __int_as_float(mt.y);
-          bmax = fmaxf(bmax, bn);
-          dblk = 2.0f * (4.7683716e-07f + 3 * J * 5.9604645e-08f) * bn + 1e-30f;
-        }
         mbar_wait_addr(a_full + 8u * buf, (unsigned)((rc / kT1Bufs) & 1));
         tc_fence_after();
         uint32_t r0[32];
@@ -352,9 +352,18 @@ __global__ void __launch_bounds__(kT1Threads, kT1CtasPerSm) k_tc_pass1(GridParam
         sx = t;
       };
       const int nfull = N / kT1Cols;  // full blocks; a partial one follows if N % 32
+      // chunk by chunk (the chunk's scale read once), block by block
 #pragma unroll 1
-      for (int kb = 0; kb < nfull; ++kb) block(kb, 32);
-      if (nfull < nblk) block(nfull, N - nfull * kT1Cols);
+      for (int kb0 = 0; kb0 < nfull; kb0 += QB) {
+        chunk_meta(kb0 / QB);
+        const int kb1 = min(nfull, kb0 + QB);
+#pragma unroll 1
+        for (int kb = kb0; kb < kb1; ++kb) block(kb, 32);
+      }
+      if (nfull < nblk) {
+        if (nfull % QB == 0) chunk_meta(nfull / QB);
+        block(nfull, N - nfull * kT1Cols);
+      }
 
       // ------------------------------------------------ per-pixel finish
       // |h~'' - h''| <= delta: fp16 split (2^-21 relative per operand pair) plus
