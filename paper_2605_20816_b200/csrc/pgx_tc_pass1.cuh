@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kT1Threads, kT1CtasPerSm) k_tc_pass1(GridParam
       for (int ci = 0; ci < nimg; ++ci)
         for (int j = 0; j < nl; ++j, ++gl) {
           const int slot = gl % L::RING;
-          mbar_wait(&bar_imgfree[slot], (unsigned)((gl / L::RING) & 1) ^ 1u);
+          mbar_wait_sleep(&bar_imgfree[slot], (unsigned)((gl / L::RING) & 1) ^ 1u);  // sleeps: no issue slots taken from the epilogue
           if (leader) {
             int s = 0;
             while (js[s] != j) ++s;  // first tile slot of distinct line j
