@@ -15,7 +15,8 @@ from .errors import NumericalError, ResourceError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(HERE, "lib")
-LIB_PATH = os.path.join(LIB_DIR, "libpgx.so")
+# PGX_LIB: an alternative in-tree build (A/B kernel experiments, tools/)
+LIB_PATH = os.environ.get("PGX_LIB") or os.path.join(LIB_DIR, "libpgx.so")
 
 PGX_OK = 0
 PGX_ERR_INVALID_ARGUMENT = 1

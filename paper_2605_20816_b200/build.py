@@ -51,6 +51,7 @@ def _compile(unit: tuple[str, str | None]) -> tuple[str, int, str]:
     src, subset = unit
     obj = os.path.join(OBJ_DIR, src[:-3] + (f".{subset}" if subset else "") + ".o")
     extra = [f"-DPGX_INST_SET={subset}"] if subset else []
+    extra += os.environ.get("PGX_XFLAGS", "").split()  # experiment defines (tools/mkvar.sh)
     cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     t0 = time.time()
     proc = subprocess.run(cmd, capture_output=True, text=True)

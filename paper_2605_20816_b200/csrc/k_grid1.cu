@@ -1,16 +1,17 @@
 // k_grid1.cu — regular-grid fp64 pass 1; launchers declared in pgx_launch.cuh.
 #include "pgx_grid.cuh"
+#include "pgx_launch.cuh"
 
 namespace pgx {
 
 template <int DIM, int D>
 void grid_dispatch_pass1(const GridParams& g, int R, int blocks, cudaStream_t s) {
   if (R == 4)
-    k_grid_pass1<DIM, D, 4><<<blocks, kG1Threads, 0, s>>>(g);
+    launch_pdl(k_grid_pass1<DIM, D, 4>, dim3(blocks), dim3(kG1Threads), 0, s, g);
   else if (R == 2)
-    k_grid_pass1<DIM, D, 2><<<blocks, kG1Threads, 0, s>>>(g);
+    launch_pdl(k_grid_pass1<DIM, D, 2>, dim3(blocks), dim3(kG1Threads), 0, s, g);
   else
-    k_grid_pass1<DIM, D, 1><<<blocks, kG1Threads, 0, s>>>(g);
+    launch_pdl(k_grid_pass1<DIM, D, 1>, dim3(blocks), dim3(kG1Threads), 0, s, g);
 }
 
 #define PGX_I(DIM, D) template void grid_dispatch_pass1<DIM, D>(const GridParams&, int, int, cudaStream_t);

@@ -1,5 +1,6 @@
 // k_grid2.cu — regular-grid fp64 pass 2; launchers declared in pgx_launch.cuh.
 #include "pgx_grid.cuh"
+#include "pgx_launch.cuh"
 
 namespace pgx {
 
@@ -11,7 +12,7 @@ static void launch_grid_pass2_gt(const GridParams& g, dim3 grid, int smem, cudaS
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     configured = true;
   }
-  kern<<<grid, kG2Threads, smem, s>>>(g);
+  launch_pdl(kern, grid, dim3(kG2Threads), smem, s, g);
 }
 
 template <int DIM, int D>

@@ -6,7 +6,7 @@ namespace pgx {
 
 template <int DIM, int D>
 void launch_tail(const EvalParams& prm, const TailParams& tp, int blocks, cudaStream_t s) {
-  k_tail<DIM, D><<<blocks, kTailThreads, 0, s>>>(prm, tp);
+  launch_pdl(k_tail<DIM, D>, dim3(blocks), dim3(kTailThreads), 0, s, prm, tp);
 }
 
 #define PGX_I(DIM, D) \

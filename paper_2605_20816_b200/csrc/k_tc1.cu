@@ -1,5 +1,6 @@
 // k_tc1.cu — tensor-core pass 1; launcher declared in pgx_launch.cuh.
 #include "pgx_grid.cuh"
+#include "pgx_launch.cuh"
 
 namespace pgx {
 
@@ -12,7 +13,7 @@ void tc_dispatch_pass1(const GridParams& g, int blocks, cudaStream_t s) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     configured = true;
   }
-  kern<<<blocks, kT1Threads, smem, s>>>(g);
+  launch_pdl(kern, dim3(blocks), dim3(kT1Threads), smem, s, g);
 }
 
 #define PGX_I(DIM, D) template void tc_dispatch_pass1<DIM, D>(const GridParams&, int, cudaStream_t);

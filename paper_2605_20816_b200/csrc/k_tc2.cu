@@ -1,5 +1,6 @@
 // k_tc2.cu — tensor-core pass 2 and the per-evaluation operand tables; launchers declared in pgx_launch.cuh.
 #include "pgx_grid.cuh"
+#include "pgx_launch.cuh"
 
 namespace pgx {
 
@@ -26,7 +27,7 @@ void tc_dispatch_pass2(const GridParams& g, dim3 grid, cudaStream_t s) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     configured = true;
   }
-  kern<<<grid, kTc2Threads, smem, s>>>(g);
+  launch_pdl(kern, grid, dim3(kTc2Threads), smem, s, g);
 }
 
 #define PGX_I(DIM, D) \

@@ -32,6 +32,18 @@ struct AlphaTable {
 
 // Pixel-centre coordinate of 0-based index k on a (2M) axis: -1 + (k+1 - 1/2)/M
 // (geometry.py:68), evaluated without contraction.
+// Programmatic dependent launch (PDL): a kernel launched with the
+// programmatic-serialization attribute may start while its predecessor in the
+// stream is still running; griddep_wait() blocks until that predecessor has
+// completed and its writes are visible. Every kernel launched that way calls
+// it before its first global access that depends on (or is read by) the
+// predecessor; without the attribute it returns at once.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// lets the dependent grid be scheduled before this grid exits
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ double axis_coord(int64_t k, int m) {
   return __dadd_rn(-1.0, __ddiv_rn(__dsub_rn((double)(k + 1), 0.5), (double)m));
 }

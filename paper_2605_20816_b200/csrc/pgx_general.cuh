@@ -453,6 +453,7 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(EvalParams e, TailParams 
   __shared__ double sred[8][33];
   __shared__ bool last;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  griddep_wait();  // PDL: the passes before this kernel are complete
 
   // (1) exact fp64 re-scan of the queued points: min and runner-up, then the
   // smallest index within the tie tolerance (geometry.py:208-210); for the

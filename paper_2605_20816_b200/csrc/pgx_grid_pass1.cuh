@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(kG1Threads) k_grid_pass1(GridParams g) {
   const int64_t pbase = line * g.side + (int64_t)seg * kG1Threads * R;
   const int N = g.N;
   const double c = g.c;
+  griddep_wait();               // PDL: theta staged, the previous evaluation complete
+  griddep_launch_dependents();  // pass 2 is scheduled once the last wave is resident
 
   if (tid == 0) {
     double lcr[K];

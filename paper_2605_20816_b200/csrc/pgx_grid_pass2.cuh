@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(kG2Threads) k_grid_pass2(GridParams g) {
 
 #pragma unroll
   for (int k = 0; k < K; ++k) acc_s[k * kG2Threads + tid] = 0.0;
+  griddep_wait();  // PDL: pass 1's per-pixel records are complete
 
   for (int64_t line = l0; line < l1; ++line) {
     __syncthreads();

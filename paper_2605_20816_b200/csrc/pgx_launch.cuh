@@ -6,12 +6,46 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <utility>
+
 #include "pgx_general.cuh"
 #include "pgx_grid_common.cuh"
 
 namespace pgx {
 
 struct GridPlan;
+
+// PDL on (default) unless PGX_PDL=0
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PGX_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// launch `kern` with programmatic stream serialization (the kernel must call
+// griddep_wait() before touching its predecessor's data, see pgx_common.cuh)
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  if (pdl_enabled()) {
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...) == cudaSuccess) return;
+    (void)cudaGetLastError();  // not launchable this way: plain launch below
+  }
+  kern<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+}
 
 // general (any point list) path + tail: pgx_general.cuh
 template <int DIM, int D>

@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(kT1Threads, kT1CtasPerSm) k_tc_pass1(GridParam
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  griddep_wait();  // PDL: the set-up above overlaps the predecessor (k_tc_coeffs)
   const unsigned tmem = tmem_base;
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
 
@@ -445,6 +446,9 @@ __global__ void __launch_bounds__(kT1Threads, kT1CtasPerSm) k_tc_pass1(GridParam
   }
   tc_fence_before();
   __syncthreads();
+  // PDL: pass 2 is scheduled once every pass-1 CTA is past its main loop (it
+  // sets up, then waits for this grid to complete)
+  griddep_launch_dependents();
   if (tid == 0) {
     double s_ell = 0.0, s_e0 = 0.0;
     long long s_cor = 0, s_amb = 0, s_nf = 0;

@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  griddep_wait();  // PDL: pass 1's records, fix lists and partials are complete
   const unsigned tmem = tmem_base;
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
   auto group_last = [&](const Tc2Cursor& c) {

@@ -403,3 +403,41 @@ def test_tc_line_chunks_match_single_launch(pgb, monkeypatch):
     assert a.e0 == pytest.approx(b.e0, rel=1e-12)
     base.close()
     ch.close()
+
+
+_PDL_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2605_20816_b200 as pgb
+from paper_2605_20816_b200 import configs
+w = configs.make("c2", labeler="gpu")
+th = np.asarray(w.theta_bench, dtype=np.float64)
+out = {{}}
+for prec in ("fp64", "tc"):
+    pr = pgb.Problem(w.grid, w.kind, w.degree, w.n_grains, w.labels0, precision=prec)
+    for rep in range(3):  # back-to-back evaluations: the overlap crosses evaluations too
+        r, s = pr.eval(th * (1 + 0.01 * rep), w.eps, lam=w.lam, want_assign=True)
+        out[f"{{prec}}{{rep}}"] = np.concatenate([[r.phi, r.err, r.e0, s.n_ambiguous], r.grad.ravel()])
+    pr.close()
+np.savez({path!r}, **out)
+"""
+
+
+def test_pdl_on_off_bitwise(pgb, tmp_path):
+    """Programmatic dependent launch (kernels set up while their predecessor
+    drains, pgx_launch.cuh) changes no result bit: a child process with
+    PGX_PDL=0 gives identical Φ, ∇, err, e0 in both fast modes."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("0", "1"):
+        path = str(tmp_path / f"pdl{flag}.npz")
+        env = dict(os.environ, PGX_PDL=flag)
+        subprocess.run([sys.executable, "-c", _PDL_CHILD.format(root=root, path=path)], env=env,
+                       check=True, timeout=600)
+        res[flag] = np.load(path)
+    for key in res["0"].files:
+        np.testing.assert_array_equal(res["0"][key], res["1"][key], err_msg=key)
