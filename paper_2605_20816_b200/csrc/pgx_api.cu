@@ -180,8 +180,10 @@ EvalParams make_params(pgx_problem* pb, double eps) {
 }
 
 // theta (host or device, f32 or f64) -> the fp64 pointer the kernels read.
+// With `out32` (the tc grid path) an fp32 theta is not converted here: k_tc_coeffs
+// reads it and writes the fp64 copy *out (one launch less per evaluation).
 pgx_status stage_theta(pgx_problem* pb, const void* theta, uint32_t flags, const double** out,
-                       int* launches) {
+                       int* launches, const float** out32 = nullptr) {
   const size_t KN = (size_t)pb->K * pb->N;
   const bool f32 = flags & PGX_THETA_F32;
   const bool dev = flags & PGX_DEVICE_PTRS;
@@ -199,6 +201,11 @@ pgx_status stage_theta(pgx_problem* pb, const void* theta, uint32_t flags, const
       *out = static_cast<const double*>(pb->d_theta_in);
       return PGX_OK;
     }
+  }
+  if (out32) {
+    *out32 = static_cast<const float*>(src);
+    *out = pb->d_theta;
+    return PGX_OK;
   }
   const int blocks = (int)std::min<size_t>((KN + 255) / 256, 1024);
   k_theta_to_f64<<<blocks, 256, 0, pb->stream>>>(src, 1, (int64_t)KN, pb->d_theta);
@@ -457,13 +464,16 @@ pgx_status pgx_eval(pgx_problem* pb, const void* theta, double eps, double lambd
   int launches = 0;
   pb->prof_reset();
   const double* theta64 = nullptr;
-  pgx_status st = stage_theta(pb, theta, flags, &theta64, &launches);
+  const float* theta32 = nullptr;
+  const bool fuse32 = pb->grid.enabled && pb->grid.tc && (flags & PGX_THETA_F32);
+  pgx_status st = stage_theta(pb, theta, flags, &theta64, &launches, fuse32 ? &theta32 : nullptr);
   if (st != PGX_OK) return st;
 
   // counters (fix-up list, non-finite, ticket) are zero here: zeroed at
   // creation and re-armed by the last CTA of the tail kernel.
   EvalParams prm = make_params(pb, eps);
   prm.theta = theta64;
+  prm.theta32 = theta32;
   double* grad_dst = dev ? grad_out : pb->d_grad;
   pgx_stats* stats_dst = dev ? stats_out : pb->d_stats;
   int blocks1 = pb->blocks1;

@@ -32,6 +32,7 @@ struct EvalParams {
   const double* __restrict__ pts;
   const int32_t* __restrict__ labels;
   const double* __restrict__ theta;  // K x N fp64
+  const float* __restrict__ theta32;  // tc grid path: fp32 source converted by k_tc_coeffs
   double eps;
   double inv_eps;
   double tau_amb;

@@ -87,6 +87,9 @@ struct GridParams {
   double eps;
   double c;        // log2(e) / eps
   double tau_amb;
+  // fp32 theta of this evaluation (nullptr: theta is fp64): k_tc_coeffs reads
+  // it directly and, on line 0, writes the fp64 copy `theta` for the kernels after it
+  const float* __restrict__ theta32;
   // outputs / scratch
   double* pix_m;   // min cost (h units) for the arg-min fix-up
   double* pix_w;   // w: p_i / 2 = 2^(w - h''_i) with w - h'' <= -1
@@ -137,8 +140,8 @@ __device__ __forceinline__ void line_factors(int64_t line, const GridParams& g,
 }
 
 // B''_{j,i} = c * sum_{k: alpha_fast(k) = j} theta_{k,i} lc[k]   (fixed order)
-template <int DIM, int D>
-__device__ __forceinline__ void line_coeffs(const double* __restrict__ theta, int N, int i,
+template <int DIM, int D, typename T>
+__device__ __forceinline__ void line_coeffs(const T* __restrict__ theta, int N, int i,
                                             const double lc[feature_count(DIM, D)], double c,
                                             double B[D + 1]) {
   constexpr int K = feature_count(DIM, D);
@@ -147,7 +150,7 @@ __device__ __forceinline__ void line_coeffs(const double* __restrict__ theta, in
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const int j = alpha_of(DIM, D, k, DIM - 1);
-    B[j] = fma(__ldg(theta + (int64_t)k * N + i), lc[k], B[j]);
+    B[j] = fma((double)__ldg(theta + (int64_t)k * N + i), lc[k], B[j]);  // fp32 theta: exact widening
   }
 #pragma unroll
   for (int j = 0; j <= D; ++j) B[j] *= c;

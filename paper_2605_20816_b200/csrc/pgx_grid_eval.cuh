@@ -52,6 +52,7 @@ inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool wa
   g.eps = e.eps;
   g.c = 1.4426950408889634074 / e.eps;
   g.tau_amb = e.tau_amb;
+  g.theta32 = gp.tc ? e.theta32 : nullptr;
 
   g.pix_m = e.pix_m;
   g.pix_w = gp.pix_w;

@@ -59,7 +59,17 @@ __global__ void __launch_bounds__(kTcCoefChunk) k_tc_coeffs(GridParams g, double
   __syncthreads();
   double B[J];
   if (i < g.N) {
-    line_coeffs<DIM, D>(g.theta, g.N, i, lc, g.c, B);
+    if (g.theta32) {
+      line_coeffs<DIM, D>(g.theta32, g.N, i, lc, g.c, B);
+      if (line == 0) {  // the fp64 theta every later kernel reads
+        double* th64 = const_cast<double*>(g.theta);
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+          th64[(int64_t)k * g.N + i] = (double)g.theta32[(int64_t)k * g.N + i];
+      }
+    } else {
+      line_coeffs<DIM, D>(g.theta, g.N, i, lc, g.c, B);
+    }
     double* out = coef + (line * g.N + i) * J;
 #pragma unroll
     for (int j = 0; j < J; ++j) out[j] = B[j];

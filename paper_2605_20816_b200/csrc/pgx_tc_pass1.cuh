@@ -307,9 +307,12 @@ __global__ void __launch_bounds__(kT1Threads, kT1CtasPerSm) k_tc_pass1(GridParam
           if (mbs < m2b) {
             // candidate columns of the block: within 2 delta + tie band of its min
             const float thr = (mbs + 2.0f * dblk + bandf * (1.0f + fabsf(mbs) * inv_cf) * 1.001f) * rinv;
-            unsigned mk = 0u;
+            // bit e of nm = sign of thr - w_e (exact: no FTZ, gradual underflow), i.e.
+            // w_e > thr or w_e = +inf padding; two instructions per column
+            unsigned nm = 0u;
 #pragma unroll
-            for (int e = 0; e < 32; ++e) mk |= (w[e] <= thr) ? (1u << e) : 0u;
+            for (int e = 31; e >= 0; --e) nm = __funnelshift_l(__float_as_uint(__fsub_rn(thr, w[e])), nm, 1);
+            const unsigned mk = ~nm;
             m3b = m2b;
             if (mbs < m1) {
               m2b = m1;
