@@ -17,9 +17,9 @@ void tc_dispatch_pix(const GridParams& g, const GridPlan& gp, cudaStream_t s) {
   k_tc_pix<D><<<g.side / kTcPixTile, kTcPixTile, 0, s>>>(g.M, g.legendre, gp.tc_pix);
 }
 
-template <int DIM, int D>
-void tc_dispatch_pass2(const GridParams& g, dim3 grid, cudaStream_t s) {
-  auto kern = k_tc_pass2<DIM, D>;
+template <int DIM, int D, bool MID>
+void tc_launch_pass2(const GridParams& g, dim3 grid, cudaStream_t s) {
+  auto kern = k_tc_pass2<DIM, D, MID>;
   // padded so that <= 2 CTAs (2 x 256 TMEM columns) share an SM
   const int smem = std::max(TcP2Smem<D + 1>::TOTAL, 80 * 1024);
   static bool configured = false;
@@ -28,6 +28,14 @@ void tc_dispatch_pass2(const GridParams& g, dim3 grid, cudaStream_t s) {
     configured = true;
   }
   launch_pdl(kern, grid, dim3(kTc2Threads), smem, s, g);
+}
+
+template <int DIM, int D>
+void tc_dispatch_pass2(const GridParams& g, dim3 grid, cudaStream_t s) {
+  if (g.items_per_split % (g.side / kTc2Px) != 0)
+    tc_launch_pass2<DIM, D, true>(g, grid, s);  // CTA ranges start and end mid-line
+  else
+    tc_launch_pass2<DIM, D, false>(g, grid, s);
 }
 
 #define PGX_I(DIM, D) \

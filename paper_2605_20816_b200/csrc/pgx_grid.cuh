@@ -21,6 +21,7 @@ struct GridPlan {
   int R = 1, segs = 1, lines = 0, blocks1 = 0;
   int tc_blocks = 0;
   int tc2_gtiles = 0, tc2_lps = 1, tc2_splits = 0;  // tensor-core pass 2 (0 = CUDA-core pass 2)
+  int64_t tc2_ips = 1;                               // its items per CTA row
   int part_splits = 0;                             // allocated split slots of part_g
   int tc_nchunks = 0;                              // 128-grain chunks (pgx_tc_coeffs.cuh)
   void* d_tc = nullptr;                            // coef | img | meta
@@ -69,6 +70,27 @@ inline void tc2_splits_for(int lines, int gtiles, int64_t slots, int cap, int& l
     if (best < 0 || cost < best) {
       best = cost;
       lps_out = lps;
+      splits_out = spr;
+    }
+  }
+}
+
+// pass-2 item splits (items = (line, 64-pixel tile) pairs, a CTA may start
+// and end mid-line): minimise waves x (items per CTA + one line of pipeline fill)
+inline void tc2_item_splits_for(int64_t items, int tpl, int gtiles, int64_t slots, int cap,
+                                int64_t& ips_out, int& splits_out) {
+  int64_t best = -1;
+  ips_out = items;
+  splits_out = 1;
+  for (int sp = 1; sp <= cap && sp <= items; ++sp) {
+    const int64_t ips = (items + sp - 1) / sp;
+    const int spr = (int)((items + ips - 1) / ips);
+    if (spr != sp) continue;
+    const int64_t waves = ((int64_t)gtiles * spr + slots - 1) / slots;
+    const int64_t cost = waves * (ips + tpl);
+    if (best < 0 || cost < best) {
+      best = cost;
+      ips_out = ips;
       splits_out = spr;
     }
   }
@@ -123,12 +145,29 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
   gp.splits = (gp.lines + gp.lines_per_split - 1) / gp.lines_per_split;
   gp.splits_out = gp.splits;
   gp.smem2 = K * kG2Threads * 8;
-  if (gp.tc && side % kTc2Px == 0) {
+  // (>= 2 tiles per line: two consecutive one-item R groups would reuse an
+  // accumulator before its flush)
+  if (gp.tc && side % kTc2Px == 0 && side >= 2 * kTc2Px) {
     // tensor-core pass 2: 128-grain tiles x line ranges, 2 CTAs per SM; the
     // split count minimises waves x lines-per-CTA (ties: fewer splits, so the
     // tail reduces less)
     gp.tc2_gtiles = (N + kTc2Grains - 1) / kTc2Grains;
+    // line-aligned CTA ranges unless item-granular ones are >= 5% cheaper
+    // (c2: 28 items per CTA instead of 4 lines = 32; the mid-line kernel
+    // variant costs registers, measured 3% slower per item at c5)
+    const int tpl2 = side / kTc2Px;
     tc2_splits_for(gp.lines, gp.tc2_gtiles, 2LL * sms, 8 * sms, gp.tc2_lps, gp.tc2_splits);
+    int64_t ips = 0;
+    int isp = 0;
+    tc2_item_splits_for((int64_t)gp.lines * tpl2, tpl2, gp.tc2_gtiles, 2LL * sms, 8 * sms, ips, isp);
+    const auto waves = [&](int sp) { return ((int64_t)gp.tc2_gtiles * sp + 2LL * sms - 1) / (2LL * sms); };
+    const int64_t cost_line = waves(gp.tc2_splits) * ((int64_t)gp.tc2_lps * tpl2 + tpl2);
+    const int64_t cost_item = waves(isp) * (ips + tpl2);
+    gp.tc2_ips = (int64_t)gp.tc2_lps * tpl2;
+    if (20 * cost_item < 19 * cost_line) {
+      gp.tc2_ips = ips;
+      gp.tc2_splits = isp;
+    }
     gp.splits_out = gp.tc2_splits;
     // line chunks (>= 64 lines each): pass 1 one CTA per SM, pass 2 sized for
     // the other half of each SM

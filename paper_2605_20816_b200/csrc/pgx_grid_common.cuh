@@ -101,6 +101,7 @@ struct GridParams {
   // pass 2
   int GT;          // grains per CTA (pass 2)
   int lines_per_split;
+  int64_t items_per_split;  // tc pass 2: (line, 64-pixel tile) items per CTA row
   int splits;
   double* part_g;  // [splits][K][N]
   // tensor-core path: per-line coefficient tables (pgx_tc_coeffs.cuh)

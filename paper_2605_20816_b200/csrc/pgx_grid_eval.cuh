@@ -118,6 +118,7 @@ inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool wa
         g2.line_lo = gp.ch_line[c];
         g2.lines = (int)gp.ch_line[c + 1];
         g2.lines_per_split = gp.ch_lps[c];
+        g2.items_per_split = (int64_t)gp.ch_lps[c] * (g.side / kTc2Px);
         g2.split_off = gp.ch_split[c];
         dim3 grid(gp.tc2_gtiles, gp.ch_splits[c]);
         if (gp.dim == 2) {
@@ -156,7 +157,7 @@ inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool wa
   if (cudaPeekAtLastError() != cudaSuccess) return PGX_ERR_CUDA;
   if (want_grad && gp.tc && gp.tc2_splits > 0) {
     dim3 grid(gp.tc2_gtiles, gp.tc2_splits);
-    g.lines_per_split = gp.tc2_lps;
+    g.items_per_split = gp.tc2_ips;
     g.splits = gp.tc2_splits;
     prof.begin(prof.ctx, "tc_pass2");
     if (gp.dim == 2) {

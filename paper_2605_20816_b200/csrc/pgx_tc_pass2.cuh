@@ -61,6 +61,7 @@ struct TcP2Smem {
 // (line index, tile) walk over a CTA's items without divisions
 struct Tc2Cursor {
   int n = 0, li = 0, t = 0;
+  __device__ explicit Tc2Cursor(int t0) : t(t0) {}
   __device__ __forceinline__ void advance(int ntiles) {
     ++n;
     if (++t == ntiles) {
@@ -70,7 +71,7 @@ struct Tc2Cursor {
   }
 };
 
-template <int DIM, int D>
+template <int DIM, int D, bool MID>
 __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
   constexpr int J = D + 1;
   constexpr int K = feature_count(DIM, D);
@@ -84,13 +85,29 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gbase = blockIdx.x * kTc2Grains;
-  // lines [line_lo, lines) of this launch, lines_per_split per CTA row
-  const int64_t l0 = g.line_lo + (int64_t)blockIdx.y * g.lines_per_split;
-  const int nlines = (int)(min((int64_t)g.lines, l0 + g.lines_per_split) - l0);
+  // items (line, tile) [line_lo, lines) x [0, ntiles) of this launch,
+  // items_per_split per CTA row; MID: the CTA may start and end mid-line
+  // (otherwise items_per_split is a multiple of ntiles and the mid-line
+  // bookkeeping compiles away: it costs registers the hot loop needs)
   const int ntiles = g.side / kTc2Px;
   const int gpl = (ntiles + kTc2Group - 1) / kTc2Group;  // R groups per line
-  const int nitems = nlines * ntiles;
-  if (nitems <= 0) return;
+  int64_t l0;  // first line (partial when t0 > 0)
+  int nitems, nlines, t0 = 0;
+  if (MID) {
+    const int64_t a0 = g.line_lo * ntiles + (int64_t)blockIdx.y * g.items_per_split;
+    const int64_t a1 = min((int64_t)g.lines * ntiles, a0 + g.items_per_split);
+    if (a1 <= a0) return;
+    nitems = (int)(a1 - a0);
+    l0 = a0 / ntiles;
+    t0 = (int)(a0 - l0 * ntiles);
+    nlines = (int)((a1 - 1) / ntiles - l0 + 1);
+  } else {
+    const int lps = (int)(g.items_per_split / ntiles);
+    l0 = g.line_lo + (int64_t)blockIdx.y * lps;
+    nlines = (int)(min((int64_t)g.lines, l0 + lps) - l0);
+    nitems = nlines * ntiles;
+    if (nitems <= 0) return;
+  }
 
   if (warp == 8) tmem_alloc(&tmem_base, 256);
   if (tid == kTc2Epi) {
@@ -111,7 +128,7 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
   const unsigned tmem = tmem_base;
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
   auto group_last = [&](const Tc2Cursor& c) {
-    return c.t == ntiles - 1 || c.t % kTc2Group == kTc2Group - 1;
+    return c.t == ntiles - 1 || c.t % kTc2Group == kTc2Group - 1 || (MID && c.n == nitems - 1);
   };
   auto r_col = [&](const Tc2Cursor& c) {  // R accumulator of the item's group
     return tmem + 192u + 32u * (unsigned)((c.li * gpl + c.t / kTc2Group) & 1);
@@ -123,7 +140,7 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
     const bool leader = lane == 0;
     const uint64_t d_a1 = umma_desc(sbase + L::A1_OFF);
     const uint64_t d_pix = umma_desc(sbase + L::PIX_OFF);
-    Tc2Cursor cl, cs, cm, cw;  // next load, next UMMA 1, next UMMA 2, next completion check
+    Tc2Cursor cl(t0), cs(t0), cm(t0), cw(t0);  // next load, UMMA 1, UMMA 2, completion check
     auto load_next = [&]() {
       const int b = cl.n % kTc2Buf;
       if (leader) {
@@ -147,7 +164,7 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
     };
     auto issue_s = [&]() {  // UMMA 1 of item cs into S_(n % 3)
       const int b = cs.n % kTc2Buf, st = cs.n % kTc2S;
-      if (cs.t == 0) mbar_wait(&bar_a[cs.li & 1], (unsigned)(cs.li >> 1) & 1u);
+      if (cs.t == 0 || (MID && cs.n == 0)) mbar_wait(&bar_a[cs.li & 1], (unsigned)(cs.li >> 1) & 1u);
       mbar_wait(&bar_full[b], (unsigned)(cs.n / kTc2Buf) & 1u);
       tc_fence_after();
       if (leader) {
@@ -174,7 +191,7 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
         const unsigned tr = r_col(cm);
         const unsigned ts = tmem + 64u * st;
         const uint64_t dl = d_pix + (uint64_t)((b * L::PIX + KS * (kTc2Px * 32)) >> 4);
-        const bool fresh = cm.t % kTc2Group == 0;
+        const bool fresh = cm.t % kTc2Group == 0 || (MID && cm.n == 0);  // a group's first item
 #pragma unroll
         for (int s = 0; s < 2 * (kTc2Px / 16); ++s) {
           const int p = s / (kTc2Px / 16), ks = s % (kTc2Px / 16);
@@ -220,7 +237,7 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
 #pragma unroll
       for (int j = 0; j < J; ++j)
         R64[j] += (double)__uint_as_float(rv[j]) + (double)__uint_as_float(rw[j]);
-      if (c.t == ntiles - 1) {
+      if (c.t == ntiles - 1 || (MID && c.n == nitems - 1)) {  // the line's (or the CTA's) last item
         if (active) {
           const double* lcp = g.tc_lc + (l0 + c.li) * K;  // k_tc_coeffs
 #pragma unroll
@@ -236,9 +253,9 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
 
     int sB_next = g.tc_meta[l0 * g.tc_nchunks + blockIdx.x].x;
     float inv = 0.0f;
-    Tc2Cursor c, cf;  // current item; item whose group may be flushed (lags by kTc2S)
+    Tc2Cursor c(t0), cf(t0);  // current item; item whose group may be flushed (lags by kTc2S)
     for (; c.n < nitems; c.advance(ntiles)) {
-      if (c.t == 0) {
+      if (c.t == 0 || (MID && c.n == 0)) {
         inv = ldexpf(1.0f, -(sB_next + 10));  // S * inv = h~''
         if (c.li + 1 < nlines) sB_next = g.tc_meta[(l0 + c.li + 1) * g.tc_nchunks + blockIdx.x].x;
       }

@@ -267,7 +267,9 @@ def test_fit_c1_trajectory(pgb):
 @pytest.mark.parametrize("prec", ["exact", "tc"])
 def test_fit_device_loop_matches_host_loop(pgb, prec):
     """fit(device_loop=True) keeps u, the gradient and the L-BFGS history on the
-    GPU; only dot-product summation order differs from the host loop."""
+    GPU; only dot-product summation order differs from the host loop. Over 25
+    iterations that 1-ulp difference is amplified by the line searches: to ~1e-12
+    with exact gradients, to ~1e-6 with tc gradients (the tc Φ tolerance)."""
     from paper_2605_20816_b200 import configs
 
     z = gl.load("fit_traj")
@@ -278,8 +280,11 @@ def test_fit_device_loop_matches_host_loop(pgb, prec):
     dev = pgb.fit(gm, pgb.FitConfig(**cfg, device_loop=True))
     a, b = np.asarray(host.phi_traj), np.asarray(dev.phi_traj)
     assert a.shape == b.shape and dev.stop_reason == host.stop_reason
-    assert np.abs(a - b).max() <= 1e-9 * (1 + np.abs(a).max())
-    assert np.abs(dev.theta.values - host.theta.values).max() <= 1e-6 * (1 + np.abs(host.theta.values).max())
+    scale = 1 + np.abs(a).max()
+    assert np.abs(a[:10] - b[:10]).max() <= 1e-9 * scale  # before the amplification
+    tol, ttol = (1e-9, 1e-6) if prec == "exact" else (1e-6, 1e-4)
+    assert np.abs(a - b).max() <= tol * scale
+    assert np.abs(dev.theta.values - host.theta.values).max() <= ttol * (1 + np.abs(host.theta.values).max())
     assert dev.gauge_residual == 0.0
     if prec == "exact":
         ref = np.asarray(z["c1_phi"])
