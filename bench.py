@@ -389,7 +389,10 @@ def run_ours(args):
                        "nonempty_grains": w.n_nonempty},
             "evals_per_s": world * args.steps / t_max,
             "e2e": {"value": e2e_value, "unit": "logits/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": 1000 * t_e2e / args.steps},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": 1000 * t_e2e / args.steps,
+                    "transfers": "theta: cudaMemcpyAsync H2D from pinned host memory; gradient + "
+                                 "stats: stored by the tail kernel into mapped pinned host memory "
+                                 "(pgx_eval zero-copy results), then stream sync"},
             "roofline": roofline,
             "cpu_baseline": cpu_baseline,
             "gpu_launches": launches,

@@ -179,6 +179,18 @@ EvalParams make_params(pgx_problem* pb, double eps) {
   return prm;
 }
 
+// Device alias of a pinned, mapped host pointer (nullptr for pageable memory).
+constexpr size_t kZeroCopyMax = 256 * 1024;
+void* host_mapped(void* p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 // theta (host or device, f32 or f64) -> the fp64 pointer the kernels read.
 // With `out32` (the tc grid path) an fp32 theta is not converted here: k_tc_coeffs
 // reads it and writes the fp64 copy *out (one launch less per evaluation).
@@ -476,6 +488,20 @@ pgx_status pgx_eval(pgx_problem* pb, const void* theta, double eps, double lambd
   prm.theta32 = theta32;
   double* grad_dst = dev ? grad_out : pb->d_grad;
   pgx_stats* stats_dst = dev ? stats_out : pb->d_stats;
+  // host results in pinned (device-mapped) memory: the tail kernel writes them
+  // over the bus directly instead of two small D2H copies (each a few us of
+  // DMA latency on the timeline); large gradients keep the copy engine
+  bool zero_copy = false;
+  if (!dev && (size_t)pb->K * pb->N * 8 <= kZeroCopyMax) {
+    void* g_dev = nullptr;
+    void* s_dev = host_mapped(stats_out);
+    if (want_grad) g_dev = host_mapped(grad_out);
+    if (s_dev && (!want_grad || g_dev)) {
+      zero_copy = true;
+      stats_dst = static_cast<pgx_stats*>(s_dev);
+      if (want_grad) grad_dst = static_cast<double*>(g_dev);
+    }
+  }
   int blocks1 = pb->blocks1;
 
   if (pb->grid.enabled) {
@@ -539,10 +565,12 @@ pgx_status pgx_eval(pgx_problem* pb, const void* theta, double eps, double lambd
   pb->last_launches = launches;
 
   if (!dev) {
-    if (want_grad)
-      PGX_CUDA(cudaMemcpyAsync(grad_out, pb->d_grad, (size_t)pb->K * pb->N * 8,
-                               cudaMemcpyDeviceToHost, s));
-    PGX_CUDA(cudaMemcpyAsync(stats_out, pb->d_stats, sizeof(pgx_stats), cudaMemcpyDeviceToHost, s));
+    if (!zero_copy) {
+      if (want_grad)
+        PGX_CUDA(cudaMemcpyAsync(grad_out, pb->d_grad, (size_t)pb->K * pb->N * 8,
+                                 cudaMemcpyDeviceToHost, s));
+      PGX_CUDA(cudaMemcpyAsync(stats_out, pb->d_stats, sizeof(pgx_stats), cudaMemcpyDeviceToHost, s));
+    }
     PGX_CUDA(cudaStreamSynchronize(s));
     if (stats_out->n_nonfinite > 0)
       return fail(PGX_ERR_NUMERICAL, "non-finite objective or gradient: phi=%g (%lld non-finite terms)",

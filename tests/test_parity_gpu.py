@@ -446,3 +446,32 @@ def test_pdl_on_off_bitwise(pgb, tmp_path):
         res[flag] = np.load(path)
     for key in res["0"].files:
         np.testing.assert_array_equal(res["0"][key], res["1"][key], err_msg=key)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "tc"])
+def test_pinned_results_zero_copy_bitwise(pgb, prec):
+    """Host results in pinned memory are written by the tail kernel through
+    the mapped alias (no D2H copies); pageable results are copied. Both give
+    identical bits, also with a host fp32 theta (the e2e bench call)."""
+    import torch
+
+    from paper_2605_20816_b200 import _lib, configs
+
+    w = configs.make("c2", labeler="gpu")
+    pr = pgb.Problem(w.grid, w.kind, w.degree, w.n_grains, w.labels0, precision=prec)
+    lib = _lib.load()
+    K, N = np.asarray(w.theta_bench).shape
+    th = np.ascontiguousarray(np.asarray(w.theta_bench, dtype=np.float32))
+    flags = _lib.PGX_WANT_GRAD | _lib.PGX_WANT_ASSIGN | _lib.PGX_THETA_F32
+    g_page, s_page = np.zeros((K, N)), np.zeros(8)
+    _lib.check(lib.pgx_eval(pr.handle, th.ctypes.data, float(w.eps), float(w.lam), flags,
+                            g_page.ctypes.data, s_page.ctypes.data))
+    th_pin = torch.from_numpy(th).pin_memory()
+    g_pin = torch.zeros((K, N), dtype=torch.float64).pin_memory()
+    s_pin = torch.zeros(8, dtype=torch.float64).pin_memory()
+    for _ in range(2):  # repeated calls reuse the mapped aliases
+        _lib.check(lib.pgx_eval(pr.handle, th_pin.data_ptr(), float(w.eps), float(w.lam), flags,
+                                g_pin.data_ptr(), s_pin.data_ptr()))
+        np.testing.assert_array_equal(g_pin.numpy(), g_page)
+        np.testing.assert_array_equal(s_pin.numpy(), s_page)
+    pr.close()
