@@ -128,7 +128,9 @@ pgx_status pgx_set_stream(pgx_problem* problem, void* stream);
  * (onehot - softmax) eta, no gauge projection) and the assignment statistics.
  * lambda >= 0 adds -lambda/2 ||theta[:, :N-1]||^2 to Phi and
  * -lambda theta[:, :N-1] to grad (lambda = 0 is the reference). grad_out may
- * be NULL when PGX_WANT_GRAD is not set. */
+ * be NULL when PGX_WANT_GRAD is not set. Without PGX_DEVICE_PTRS the call is
+ * synchronous; host result buffers in pinned (mapped) memory are written by the
+ * last kernel directly (up to 256 KB of gradient), pageable ones by copies. */
 pgx_status pgx_eval(pgx_problem* problem, const void* theta, double eps, double lambda,
                     uint32_t flags, double* grad_out, pgx_stats* stats_out);
 
