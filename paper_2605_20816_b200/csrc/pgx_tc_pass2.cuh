@@ -46,6 +46,16 @@ constexpr int kTc2S = 3;                  // S stages in TMEM (UMMA 1 runs 3 til
 constexpr int kTc2Buf = 6;                // tile buffers (pixel operands + records)
 constexpr int kTc2RecFloats = 4 * kTc2Px;  // w13[64] | wl13[64] | qn[64] | label[64]
 
+// The exponent 13 + w - h~'' is formed from the fp32-rounded w = (float)w13 and,
+// optionally, its fp32 residual wl13 (pass-1 record). The residual is below the
+// logit error itself (|w13 - w| <= 2^-24 |w13| against ~2^-22 |h''| for the
+// fp16-split logits; measured c1-c5 tc-vs-exact errors unchanged without it,
+// tools/tc_err.py), so it is dropped -- one FADD and half the record loads per
+// logit -- except in the high-degree 2-D kernels, where the register allocation
+// at the 96-register cap came out 2% slower without it (c5).
+template <int DIM, int D>
+constexpr bool kTc2WithResidual = DIM == 2 && D >= 6;
+
 template <int J>
 struct TcP2Smem {
   static constexpr int KS = tc_ksteps(J);
@@ -280,12 +290,18 @@ __global__ void __launch_bounds__(kTc2Threads, 2) k_tc_pass2(GridParams g) {
 #pragma unroll
       for (int x4 = 0; x4 < 32; x4 += 4) {
         const float4 w4 = *reinterpret_cast<const float4*>(rec + x4);
-        const float4 l4 = *reinterpret_cast<const float4*>(rec + kTc2Px + x4);
         const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
-        const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+        if constexpr (!kTc2WithResidual<DIM, D>) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e)  // p/2 * 2^13 = 2^(13 + w - h~'')
-          rr[x4 + e] = ex2_approx(fmaf(-__uint_as_float(sv[x4 + e]), inv, wv[e]) + lv[e]);
+          for (int e = 0; e < 4; ++e)  // p/2 * 2^13 = 2^(13 + w - h~'')
+            rr[x4 + e] = ex2_approx(fmaf(-__uint_as_float(sv[x4 + e]), inv, wv[e]));
+        } else {
+          const float4 l4 = *reinterpret_cast<const float4*>(rec + kTc2Px + x4);
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            rr[x4 + e] = ex2_approx(fmaf(-__uint_as_float(sv[x4 + e]), inv, wv[e]) + lv[e]);
+        }
       }
       if (lab_warp) {  // label grain: -(1 - p_G)/2 * 2^13 from pass 1 (no cancellation)
         const int* labs = reinterpret_cast<const int*>(rec) + 3 * kTc2Px;
