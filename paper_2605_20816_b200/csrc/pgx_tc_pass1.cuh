@@ -340,14 +340,16 @@ __global__ void __launch_bounds__(kT1Threads, kT1CtasPerSm) k_tc_pass1(GridParam
         const float nr = -ref;
         const int labc = lab - kb * kT1Cols;
         float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // 4 independent FADD chains
-        if (cn == 32 && !__any_sync(0xffffffffu, (unsigned)labc < 32u)) {
+        // padding columns (e >= cn) hold +inf: their terms are exactly 0, so only
+        // a block holding some lane's label column needs the masked loop
+        if (!__any_sync(0xffffffffu, (unsigned)labc < 32u)) {
 #pragma unroll
           for (int e = 0; e < 32; ++e) s4[e & 3] += ex2_approx(-fmaf(w[e], inv, nr));
         } else {
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
             const float x = ex2_approx(-fmaf(w[e], inv, nr));
-            s4[e & 3] += (e < cn && e != labc) ? x : 0.0f;
+            s4[e & 3] += e != labc ? x : 0.0f;
           }
         }
         const float y = ((s4[0] + s4[1]) + (s4[2] + s4[3])) - sxc;  // Kahan step
