@@ -288,9 +288,17 @@ __global__ void __launch_bounds__(kT1Threads, kT1CtasPerSm) k_tc_pass1(GridParam
         tmem_ld32_nowait(t_slot + buf * kT1Cols, r0);
         tmem_ld_wait();
         tmem_regs_ready(r0);
-        tc_fence_before();
-        slot_sync(s);
-        if (leader && kb + kT1Bufs < nblk) issue(kb + kT1Bufs);
+        // the slot's warps meet every second block: buffers of blocks kb - 1 and
+        // kb are then free for the refills kb + 3 and kb + 4 (issued 2 and 3
+        // blocks before their use); measured c2 -2%, c4/c5 unchanged vs every block
+        if (kb & 1) {
+          tc_fence_before();
+          slot_sync(s);
+          if (leader) {
+            if (kb + kT1Bufs - 1 < nblk) issue(kb + kT1Bufs - 1);
+            if (kb + kT1Bufs < nblk) issue(kb + kT1Bufs);
+          }
+        }
         ++rc;
         float w[32];
 #pragma unroll
