@@ -575,6 +575,13 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(EvalParams e, TailParams 
   const int b0 = tid * per, b1 = min(prm.blocks1, b0 + per);
   double ell = 0.0, e0 = 0.0;
   long long cor = 0, amb = 0, nf = 0;
+  int n_fix = 0;
+  if (tid == 0) {  // the counters, loaded alongside the partials (one round trip, not two)
+    cor = *(volatile long long*)prm.fix_correct;
+    amb = *((volatile long long*)prm.fix_correct + 1);
+    nf = prm.nonfinite_grad ? *(volatile int*)prm.nonfinite_grad : 0;
+    n_fix = *(volatile int*)e.fix_count;
+  }
 #pragma unroll 4
   for (int b = b0; b < b1; ++b) {
     ell += prm.part_d[2 * b + 0];
@@ -592,15 +599,12 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(EvalParams e, TailParams 
   if (tid == 0) {
     StatsDev* out = reinterpret_cast<StatsDev*>(prm.stats_out);
     const double P = (double)prm.P;
-    cor += *(volatile long long*)prm.fix_correct;
-    amb += *((volatile long long*)prm.fix_correct + 1);
-    nf += prm.nonfinite_grad ? *(volatile int*)prm.nonfinite_grad : 0;
     double phi = ell / P;  // objective.py:161
     if (prm.lambda != 0.0) phi -= 0.5 * prm.lambda * th2;
     out->phi = phi;
     out->err = prm.want_assign ? 1.0 - (double)cor / P : 0.0;  // objective.py:163
     out->e0 = prm.want_assign ? e0 / P : 0.0;                  // objective.py:164
-    out->n_rescanned = (double)*(volatile int*)e.fix_count;  // points re-scanned exactly
+    out->n_rescanned = (double)n_fix;  // points re-scanned exactly
     out->n_points = prm.P;
     out->n_correct = cor;
     out->n_ambiguous = amb;
