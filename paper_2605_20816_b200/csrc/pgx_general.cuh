@@ -456,58 +456,8 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(EvalParams e, TailParams 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   griddep_wait();  // PDL: the passes before this kernel are complete
 
-  // (1) exact fp64 re-scan of the queued points: min and runner-up, then the
-  // smallest index within the tie tolerance (geometry.py:208-210); for the
-  // grid path it also decides the ambiguity of these points (fix_amb).
-  // One warp per queued point, lanes over grains (coalesced theta reads).
+  // the fix-up count, loaded now so its latency overlaps phase (2)
   const int count = *e.fix_count;
-  const int nwarps = gridDim.x * (kTailThreads / 32);
-  for (int q = blockIdx.x * (kTailThreads / 32) + warp; q < count; q += nwarps) {
-    const int64_t p = e.fix_list[q];
-    double x[DIM], eta[K];
-    point_coords<DIM>(p, e.M, e.pts, x);
-    features<DIM, D>(x, e.legendre != 0, eta);
-    double m = CUDART_INF, m2 = CUDART_INF;
-    for (int i = lane; i < e.N; i += 32) {
-      double h = 0.0;
-#pragma unroll
-      for (int k = 0; k < K; ++k) h = fma(e.theta[(int64_t)k * e.N + i], eta[k], h);
-      if (h < m) {
-        m2 = m;
-        m = h;
-      } else if (h < m2) {
-        m2 = h;
-      }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {  // merge (min, runner-up) pairs
-      const double om = __shfl_xor_sync(0xffffffffu, m, off);
-      const double om2 = __shfl_xor_sync(0xffffffffu, m2, off);
-      const double nm = fmin(m, om);
-      m2 = fmin(fmax(m, om), fmin(m2, om2));
-      m = nm;
-    }
-    const double thr = tie_threshold(m);
-    int best = 0x7fffffff;
-    for (int i = lane; i < e.N; i += 32) {
-      double h = 0.0;
-#pragma unroll
-      for (int k = 0; k < K; ++k) h = fma(e.theta[(int64_t)k * e.N + i], eta[k], h);
-      if (h <= thr) {
-        best = i;
-        break;
-      }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, off));
-    if (best == 0x7fffffff) best = 0;
-    if (lane == 0) {
-      if (e.labels_out) e.labels_out[p] = best + 1;
-      if (e.labels && best == e.labels[p]) atomicAdd((unsigned long long*)e.fix_correct, 1ull);
-      if (t.fix_amb && (m2 - m) <= e.tau_amb * (1.0 + fabs(m)))
-        atomicAdd((unsigned long long*)e.fix_correct + 1, 1ull);
-    }
-  }
 
   // (2) gradient: warp w of CTA b owns entries ent = 8 b + w (grid-strided);
   // it also accumulates its entries' share of ||theta[:, :N-1]||^2 for the
@@ -560,6 +510,58 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(EvalParams e, TailParams 
 #pragma unroll
       for (int w = 0; w < kTailThreads / 32; ++w) s8 += sred[w][0];
       t.part_th2[blockIdx.x] = s8;
+    }
+  }
+
+  // (1) exact fp64 re-scan of the queued points: min and runner-up, then the
+  // smallest index within the tie tolerance (geometry.py:208-210); for the
+  // grid path it also decides the ambiguity of these points (fix_amb).
+  // One warp per queued point, lanes over grains (coalesced theta reads).
+  const int nwarps = gridDim.x * (kTailThreads / 32);
+  for (int q = blockIdx.x * (kTailThreads / 32) + warp; q < count; q += nwarps) {
+    const int64_t p = e.fix_list[q];
+    double x[DIM], eta[K];
+    point_coords<DIM>(p, e.M, e.pts, x);
+    features<DIM, D>(x, e.legendre != 0, eta);
+    double m = CUDART_INF, m2 = CUDART_INF;
+    for (int i = lane; i < e.N; i += 32) {
+      double h = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) h = fma(e.theta[(int64_t)k * e.N + i], eta[k], h);
+      if (h < m) {
+        m2 = m;
+        m = h;
+      } else if (h < m2) {
+        m2 = h;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {  // merge (min, runner-up) pairs
+      const double om = __shfl_xor_sync(0xffffffffu, m, off);
+      const double om2 = __shfl_xor_sync(0xffffffffu, m2, off);
+      const double nm = fmin(m, om);
+      m2 = fmin(fmax(m, om), fmin(m2, om2));
+      m = nm;
+    }
+    const double thr = tie_threshold(m);
+    int best = 0x7fffffff;
+    for (int i = lane; i < e.N; i += 32) {
+      double h = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) h = fma(e.theta[(int64_t)k * e.N + i], eta[k], h);
+      if (h <= thr) {
+        best = i;
+        break;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, off));
+    if (best == 0x7fffffff) best = 0;
+    if (lane == 0) {
+      if (e.labels_out) e.labels_out[p] = best + 1;
+      if (e.labels && best == e.labels[p]) atomicAdd((unsigned long long*)e.fix_correct, 1ull);
+      if (t.fix_amb && (m2 - m) <= e.tau_amb * (1.0 + fabs(m)))
+        atomicAdd((unsigned long long*)e.fix_correct + 1, 1ull);
     }
   }
 
