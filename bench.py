@@ -1,11 +1,12 @@
 """Benchmark of the fused Phi + grad + assignment evaluation (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--precision fp64]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--precision tc]
     python bench.py --impl reference ...      # CPU reference arm (oracle port)
 
 One "step" = one fused objective+gradient+assignment evaluation of the whole
 workload (the unit ``fit`` calls per trial point, optimizer.py:215-219).
-Default workload: BASELINE.json configs[1] (c2).  Multi-GPU runs are replicas
+Default workload: c5, the largest single-GPU config of BASELINE.json (the
+north_star's ">= 60% of roofline on the largest config").  Multi-GPU runs are replicas
 (the north_star forbids multi-GPU data paths): every rank evaluates
 the full workload; value = all ranks' logits / max-over-ranks time.
 """
@@ -17,9 +18,16 @@ import json
 import math
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
+
+# The CPU legs (cpu_baseline, --impl reference) parallelise the NumPy oracle
+# with a chunk thread pool; BLAS must then be single-threaded, and this has to
+# be set before the first numpy import anywhere in the process.
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("OMP_NUM_THREADS", "1")
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -39,13 +47,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     # tc: tcgen05 logits (3-product fp16 split, fp32 accumulate) -- the north-star
     # path, within the stated 1e-6 (phi) / 1e-5 (grad) tolerances; fp64 and exact
     # are the tighter modes
     ap.add_argument("--precision", default=os.environ.get("PGX_PRECISION", "tc"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    # the fp64 mode measured beside the headline mode (same problem, same theta)
+    ap.add_argument("--also", default="fp64", help="comma list of extra precision modes ('' = none)")
     return ap.parse_args()
 
 
@@ -234,7 +244,138 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ roofline
+FP64_DFMA_PER_CLK_SM = 59   # measured FP64 FMA rate on this pool's B200s (tools/)
+
+
+def roofline_8d(P, N, K, precision, t_eval_s, peaks, sm_mhz):
+    """T_roof = max(4PNK / F_mode, PN / E_exp, B / BW_HBM); frac = T_roof / t_eval.
+
+    F_mode: tc = measured bf16 burst peak / 3 (the 3-product fp16 split), fp64 /
+    exact = the FP64 FMA peak; E_exp = 16 MUFU ex2 /clk/SM x 148 x sm_max clock;
+    B = the algorithmic minimum labels 4P + theta 4KN + grad 8KN (§8d)."""
+    clk = sm_mhz * 1e6
+    flops, exps, nbytes = 4.0 * P * N * K, float(P * N), 4.0 * P + 12.0 * K * N
+    if precision == "tc":
+        f_peak, f_name = peaks["bf16_tflops"] * 1e12 / 3.0, "tensor"
+    else:
+        f_peak, f_name = 2.0 * FP64_DFMA_PER_CLK_SM * N_SMS * clk, "fp64"
+    e_peak = MUFU_PER_CLK_SM * N_SMS * clk
+    bw = peaks["hbm_gbs"] * 1e9
+    terms = {f_name: flops / f_peak, "mufu": exps / e_peak, "hbm": nbytes / bw}
+    bound = max(terms, key=terms.get)
+    t_roof = terms[bound]
+    work = {f_name: (flops / 1e12, f_peak / 1e12, "TFLOP/s"), "mufu": (exps / 1e9, e_peak / 1e9, "Gexp/s"),
+            "hbm": (nbytes / 1e9, bw / 1e9, "GB/s")}[bound]
+    return {
+        "bound": bound, "achieved": work[0] / t_eval_s, "peak": work[1], "unit": work[2],
+        "frac": t_roof / t_eval_s, "t_roof_ms": 1e3 * t_roof, "t_eval_ms": 1e3 * t_eval_s,
+        "terms_ms": {k: 1e3 * v for k, v in terms.items()},
+        "fracs": {k: v / t_eval_s for k, v in terms.items()},
+        "algorithmic": {"flops": flops, "exps": exps, "bytes": nbytes},
+        "peaks": {"F_mode_tflops": f_peak / 1e12, "E_exp_gexps": e_peak / 1e9, "hbm_gbs": bw / 1e9,
+                  "sm_mhz": sm_mhz},
+    }
+
+
+def kernel_roofline(name, ms, P, N, K, peaks, sm_mhz):
+    """The dominant kernel's own fraction: pass 1 = 2PNK flops + PN exps,
+    pass 2 = 2PNK flops + PN exps (each recomputes the logits; §8d splits the
+    4PNK evenly), other kernels: bytes only."""
+    t = ms / 1e3
+    clk = sm_mhz * 1e6
+    exps = float(P * N)
+    e_peak = MUFU_PER_CLK_SM * N_SMS * clk
+    f_peak = peaks["bf16_tflops"] * 1e12 / 3.0
+    if "pass" in name or "sweep" in name or "grad" in name:
+        return {"kernel": name, "ms": ms, "mufu_frac": exps / e_peak / t,
+                "tensor_frac": 2.0 * P * N * K / f_peak / t}
+    return {"kernel": name, "ms": ms}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+class _OracleProblem:
+    """CPU stand-in for ``Problem`` in the cpu_baseline leg: the reference fit
+    loop (optimizer.fit, a port of optimizer.py:195-342) evaluating through the
+    NumPy oracle port of objective.evaluate_objective."""
+
+    def __init__(self, w):
+        import oracle
+
+        self._o = oracle
+        self.w = w
+        self.pts = oracle.grid_points(w.M, w.dim)
+
+    def eval(self, theta, eps, *, lam=0.0, want_grad=True, want_assign=False):
+        r = self._o.evaluate_problem(theta, self.w.kind, self.w.degree, self.pts, self.w.labels0,
+                                     eps, want_grad=want_grad, want_assign=want_assign, lam=lam)
+        from paper_2605_20816_b200.objective import EvalResult
+
+        return EvalResult(r.phi, r.grad, r.err, r.e0), None
+
+
+def fit_c1(problem, precision=None):
+    """The reference fit at c1: 100 L-BFGS iterations."""
+    import paper_2605_20816_b200 as pgb
+    from paper_2605_20816_b200 import configs
+
+    w = configs.c1(labeler="host")
+    gm = pgb.GrainMap(grid=w.grid, labels=w.labels0 + 1, n_grains=w.n_grains)
+    cfg = pgb.FitConfig(degree=w.degree, basis_kind=w.kind, eps=w.eps, max_iters=100,
+                        precision=precision or "tc")
+    t0 = time.perf_counter()
+    rep = pgb.fit(gm, cfg, problem=problem(w) if callable(problem) else problem)
+    dt = time.perf_counter() - t0
+    return {"seconds": dt, "iterations": rep.iterations_run, "evaluations": rep.evaluations,
+            "evals_per_s": rep.evaluations / dt, "phi_final": rep.phi_final, "stop": rep.stop_reason}
+
+
+def cpu_baseline_leg(w, seconds):
+    """The oracle (NumPy port of polygrain.evaluate_objective) on this host's
+    cores: all threads (the reported value) and 1 thread, plus the c1 fit."""
+    threads = os.cpu_count() or 1
+    rate, desc, _, _ = cpu_measure(w, seconds, threads)
+    rate1, desc1, _, _ = cpu_measure(w, seconds / 2, 1)
+    fit = fit_c1(_OracleProblem)
+    return {"value": rate, "unit": "logits/s", "cores": threads, "kind": "port", "sample": desc,
+            "cpu_model": cpu_model(), "nproc": threads,
+            "single_thread": {"value": rate1, "unit": "logits/s", "cores": 1, "sample": desc1},
+            "fit_c1": fit}
+
+
 # ------------------------------------------------------------------ our arm
+def time_mode(prob, step, flush, stream, steps, warmup, dev):
+    """Device time per step (CUDA events on the problem's stream, L2 flushed
+    between steps outside the events)."""
+    import torch
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(warmup, 0)):
+            step()
+        torch.cuda.synchronize(dev)
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        for i in range(steps):
+            flush.zero_()
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize(dev)
+    return [a.elapsed_time(b) for a, b in zip(starts, ends)]
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -254,7 +395,7 @@ def run_ours(args):
     f32 = w.theta_dtype == "f32"
     theta_d = torch.as_tensor(np.asarray(w.theta_bench), device=dev)
     grad_d = torch.empty((K, N), dtype=torch.float64, device=dev)
-    stats_d = torch.empty(8, dtype=torch.float64, device=dev)
+    stats_d = torch.empty(_lib.STATS_WORDS, dtype=torch.float64, device=dev)
     flags = _lib.PGX_WANT_GRAD | _lib.PGX_WANT_ASSIGN | (_lib.PGX_THETA_F32 if f32 else 0)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
@@ -287,11 +428,11 @@ def run_ours(args):
     value = replica_value(world, args.steps, P * N, t_max)
     stats = stats_d.cpu().numpy()
 
-    # ---- kernel-level timing (dominant kernel) with CUDA events, same stream
+    # ---- kernel-level timing with CUDA events on the problem's stream
     prob.set_profiling(True)
     per_kernel = {}
     with torch.cuda.stream(stream):
-        for _ in range(max(3, min(args.steps, 20))):
+        for _ in range(max(3, min(args.steps, 10))):
             flush.zero_()
             step()
             for name, ms in prob.profile():
@@ -304,7 +445,7 @@ def run_ours(args):
     theta_h = torch.empty(theta_d.shape, dtype=theta_d.dtype, pin_memory=True)
     theta_h.copy_(theta_d.cpu())
     grad_h = torch.empty((K, N), dtype=torch.float64, pin_memory=True)
-    stats_h = torch.empty(8, dtype=torch.float64, pin_memory=True)
+    stats_h = torch.empty(_lib.STATS_WORDS, dtype=torch.float64, pin_memory=True)
     host_flags = flags & ~_lib.PGX_DEVICE_PTRS
     lib = _lib.load()
 
@@ -328,52 +469,49 @@ def run_ours(args):
     t_e2e = max_over_ranks(sum(e_ms) / 1000.0, world, dev)
     e2e_value = replica_value(world, args.steps, P * N, t_e2e)
     h2d = K * N * (4 if f32 else 8)
-    d2h = K * N * 8 + 64
+    d2h = K * N * 8 + 8 * _lib.STATS_WORDS
 
-    # ---- roofline of the dominant kernel
+    # ---- the other precision modes on the same workload (device-timed)
+    modes = {}
+    for m in [x for x in args.also.split(",") if x and x != args.precision]:
+        pm = pgb.Problem(w.grid, w.kind, w.degree, w.n_grains, w.labels0, precision=m,
+                         device=local, stream=stream.cuda_stream)
+
+        def step_m(pm=pm):
+            pm.eval_device(theta_d.data_ptr(), w.eps, w.lam, flags, grad_d.data_ptr(),
+                           stats_d.data_ptr())
+
+        ms = time_mode(pm, step_m, flush, stream, max(3, args.steps // 4), 2, dev)
+        t_m = sum(ms) / 1e3 / len(ms)
+        modes[m] = {"ms_per_step": 1e3 * t_m, "value": P * N / t_m, "unit": "logits/s",
+                    "dtype": DTYPE[m], "phi": float(stats_d[0].item())}
+        pm.close()
+
+    # ---- roofline (§8d, whole evaluation) + the dominant kernel
     peaks, peaks_kind = load_peaks()
     clocks = clk.summary()
-    mhz = clocks["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)
-    t_top = avg[top] / 1000.0
-    logits = P * N
-    flops_top = (2 if "pass1" in top else 4) * logits * K
-    exps_top = logits
-    bytes_top = P * 4 + K * N * 8 + (16 * P if "pass1" in top else 16 * P + 8 * K * N)
-    tensor_peak = peaks["bf16_tflops"] * 1e12
-    pipes = {
-        "fp64": {"achieved": flops_top / t_top / 1e12,
-                 "peak": 2 * DFMA_PER_CLK_SM * N_SMS * mhz * 1e6 / 1e12, "unit": "TFLOP/s"},
-        "mufu_ex2": {"achieved": exps_top / t_top / 1e9,
-                     "peak": MUFU_PER_CLK_SM * N_SMS * mhz * 1e6 / 1e9, "unit": "Gexp/s"},
-        "hbm": {"achieved": bytes_top / t_top / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s"},
-        "tensor": {"achieved": flops_top / t_top / 1e12, "peak": tensor_peak / 1e12,
-                   "unit": "TFLOP/s"},
-    }
-    for v in pipes.values():
-        v["frac"] = v["achieved"] / v["peak"]
-    binding = max(("fp64", "mufu_ex2") if args.precision != "tc" else ("tensor", "mufu_ex2"),
-                  key=lambda k: pipes[k]["frac"])
+    sm_peak = float(peaks.get("sm_max_mhz", 1965.0))
+    t_eval = t_max / args.steps
+    roofline = roofline_8d(P, N, K, args.precision, t_eval, peaks, sm_peak)
     traffic, traffic_src = measured_traffic(args.config, args.precision, top)
-    roofline = {
-        "bound": "tensor", "achieved": pipes["tensor"]["achieved"], "peak": pipes["tensor"]["peak"],
-        "unit": "TFLOP/s", "frac": pipes["tensor"]["frac"], "traffic": traffic,
-        "traffic_source": traffic_src, "algorithmic_bytes": bytes_top,
-        "kernel": top, "kernel_ms": avg[top], "kernel_share": avg[top] / (sum(avg.values())),
-        "peak_kind": f"{peaks_kind} (bf16 burst, MEASURED_PEAKS.json)",
-        "binding_pipe": binding, "binding_frac": pipes[binding]["frac"], "pipes": pipes,
+    roofline.update({
+        "traffic": traffic, "traffic_source": traffic_src,
+        "peak_kind": f"{peaks_kind} (MEASURED_PEAKS.json bf16 burst / 3; MUFU 16/clk/SM x 148 x "
+                     f"sm_max {sm_peak:.0f} MHz; HBM copy)",
+        "dominant": kernel_roofline(top, avg[top], P, N, K, peaks, sm_peak),
+        "kernel_share": avg[top] / sum(avg.values()),
         "kernels_ms": avg,
-        "note": ("algorithmic work of the dominant kernel: pass1 = 2PNK flops + PN exps, "
-                 "pass2 = 4PNK flops + PN exps; SFU/FP64 peaks = per-SM issue rate x 148 SMs x "
-                 "median SM clock under load"),
-    }
+    })
 
     cpu_baseline = None
+    fit = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-        threads = os.cpu_count() or 1
-        rate, desc, _, _ = cpu_measure(w, args.cpu_seconds, threads)
-        cpu_baseline = {"value": rate, "unit": "logits/s", "cores": threads, "kind": "port",
-                        "sample": desc}
+        cpu_baseline = cpu_baseline_leg(w, args.cpu_seconds)
+    if rank == 0 and world == 1:
+        try:
+            fit = fit_c1(None, args.precision)
+        except Exception as exc:  # noqa: BLE001
+            fit = {"error": repr(exc)}
 
     if rank == 0:
         line = {
@@ -391,15 +529,18 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": "logits/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": 1000 * t_e2e / args.steps,
                     "transfers": "theta: cudaMemcpyAsync H2D from pinned host memory; gradient + "
-                                 "stats: stored by the tail kernel into mapped pinned host memory "
-                                 "(pgx_eval zero-copy results), then stream sync"},
+                                 "stats: D2H (or, <= 256 KB, stored by the tail kernel into mapped "
+                                 "pinned host memory), then stream sync"},
             "roofline": roofline,
+            "modes": modes,
             "cpu_baseline": cpu_baseline,
+            "fit_c1_gpu": fit,
             "gpu_launches": launches,
             "clocks": clocks,
             "result": {"phi": float(stats[0]), "err": float(stats[1]), "e0": float(stats[2]),
                        "n_rescanned": int(stats[3]),
-                       "n_ambiguous": int(stats.view(np.int64)[6])},
+                       "n_ambiguous": int(stats.view(np.int64)[6]),
+                       "flags": int(stats.view(np.int64)[8])},
         }
         print(json.dumps(line), flush=True)
     prob.close()
@@ -430,8 +571,25 @@ def measured_traffic(config: str, precision: str, kernel: str):
 DTYPE = {"tc": "f16x3-f32", "fp64": "f64", "exact": "f64"}
 
 
+def self_launch(args) -> bool:
+    """`bench.py --gpus N` without torchrun: launch the N ranks ourselves
+    (one process per GPU, the driver's own torchrun form)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    self_launch(args)
     if args.impl == "reference":
         run_reference(args)
     else:

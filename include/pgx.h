@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define PGX_ABI_VERSION 1
+#define PGX_ABI_VERSION 2
 
 typedef enum {
     PGX_OK = 0,
@@ -106,7 +106,18 @@ typedef struct {
     int64_t n_correct;     /* pixels whose tie-tolerant arg-min equals G       */
     int64_t n_ambiguous;   /* pixels whose top-2 margin <= tau (1 + |min|)     */
     int64_t n_nonfinite;   /* non-finite Phi / grad contributions seen         */
+    int64_t flags;         /* PGX_STAT_* bits                                  */
 } pgx_stats;
+
+/* pgx_stats.flags.  PGX_STAT_RANGE: a fast mode (FP64 / TC) evaluated a theta
+ * whose logit range max_i sum_k |theta_ki| / (eps ln 2) exceeds 2^16, beyond
+ * which the fp32 / fp16-split logits no longer meet the stated tolerances.
+ * With host pointers pgx_eval never returns it: it evaluates such a theta on
+ * the exact kernels instead (PGX_PREC_EXACT arithmetic).  With
+ * PGX_DEVICE_PTRS the check runs on the device and the caller re-evaluates
+ * (the Python device loop does so on a PGX_PREC_EXACT problem). */
+enum { PGX_STAT_RANGE = 1 };
+#define PGX_FAST_RANGE 65536.0
 
 typedef struct pgx_problem pgx_problem;
 
@@ -149,6 +160,14 @@ pgx_status pgx_assign(pgx_problem* problem, const void* theta, uint32_t flags,
 pgx_status pgx_label_moments(int resolution, int64_t n_points, const int64_t* labels0, int n_grains,
                              int64_t* out);
 const char* pgx_label_moments_error(void);
+
+/* Which kernel family pgx_eval runs for this problem (fixed at creation):
+ * PGX_PATH_GENERAL (fp64 CUDA-core kernels over any point list; the exact
+ * mode, and the fallback of the fast modes where the grid paths do not
+ * apply), PGX_PATH_GRID_FP64 (separable regular-grid kernels) or
+ * PGX_PATH_GRID_TC (tcgen05 regular-grid kernels). */
+enum { PGX_PATH_GENERAL = 0, PGX_PATH_GRID_FP64 = 1, PGX_PATH_GRID_TC = 2 };
+int pgx_problem_path(pgx_problem* problem);
 
 /* Number of kernel launches the last pgx_eval / pgx_assign enqueued. */
 int pgx_last_launch_count(pgx_problem* problem);

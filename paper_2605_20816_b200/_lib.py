@@ -37,6 +37,16 @@ PGX_WANT_ASSIGN = 2
 PGX_DEVICE_PTRS = 4
 PGX_THETA_F32 = 8
 
+PGX_STAT_RANGE = 1  # pgx_stats.flags: theta beyond the fast modes' logit range
+PGX_FAST_RANGE = 65536.0
+ABI_VERSION = 2
+STATS_WORDS = 9  # sizeof(pgx_stats) / 8
+
+PGX_PATH_GENERAL = 0
+PGX_PATH_GRID_FP64 = 1
+PGX_PATH_GRID_TC = 2
+PATH_NAMES = {PGX_PATH_GENERAL: "general", PGX_PATH_GRID_FP64: "grid_fp64", PGX_PATH_GRID_TC: "grid_tc"}
+
 PGX_MEM_HOST = 0
 PGX_MEM_DEVICE = 1
 
@@ -68,6 +78,7 @@ class PgxStats(ctypes.Structure):
         ("n_correct", c_int64),
         ("n_ambiguous", c_int64),
         ("n_nonfinite", c_int64),
+        ("flags", c_int64),
     ]
 
 
@@ -82,6 +93,7 @@ SIGNATURES = {
     "pgx_eval": (c_int, [c_void_p, c_void_p, c_double, c_double, c_uint32, c_void_p, c_void_p]),
     "pgx_assign": (c_int, [c_void_p, c_void_p, c_uint32, c_void_p, c_void_p, c_void_p]),
     "pgx_last_launch_count": (c_int, [c_void_p]),
+    "pgx_problem_path": (c_int, [c_void_p]),
     "pgx_set_profiling": (c_int, [c_void_p, c_int]),
     "pgx_profile_count": (c_int, [c_void_p]),
     "pgx_profile_name": (c_char_p, [c_void_p, c_int]),
@@ -108,7 +120,7 @@ def load():
         fn = getattr(lib, name)
         fn.restype = restype
         fn.argtypes = argtypes
-    if lib.pgx_abi_version() != 1:
+    if lib.pgx_abi_version() != ABI_VERSION:
         raise RuntimeError("libpgx.so ABI version mismatch")
     _lib = lib
     return lib

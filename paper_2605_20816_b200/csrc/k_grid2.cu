@@ -7,11 +7,8 @@ namespace pgx {
 template <int DIM, int D, int GT>
 static void launch_grid_pass2_gt(const GridParams& g, dim3 grid, int smem, cudaStream_t s) {
   auto kern = k_grid_pass2<DIM, D, GT>;
-  static bool configured = false;  // static + dynamic shared memory may exceed 48 KB
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    configured = true;
-  }
+  static DeviceOnce once;  // static + dynamic shared memory may exceed 48 KB
+  once.run([&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024); });
   launch_pdl(kern, grid, dim3(kG2Threads), smem, s, g);
 }
 

@@ -6,7 +6,7 @@ namespace pgx {
 
 template <int DIM, int D>
 void tc_dispatch_coeffs(const GridParams& g, const GridPlan& gp, cudaStream_t s) {
-  dim3 grid(gp.tc_nchunks, gp.lines);
+  dim3 grid(gp.lines, gp.tc_nchunks);
   k_tc_coeffs<DIM, D><<<grid, kTcCoefChunk, 0, s>>>(g, gp.tc_coef, gp.tc_img,
                                                     reinterpret_cast<TcCoefMeta*>(gp.tc_meta),
                                                     gp.tc_nchunks);
@@ -22,11 +22,8 @@ void tc_launch_pass2(const GridParams& g, dim3 grid, cudaStream_t s) {
   auto kern = k_tc_pass2<DIM, D, MID>;
   // padded so that <= 2 CTAs (2 x 256 TMEM columns) share an SM
   const int smem = std::max(TcP2Smem<D + 1>::TOTAL, 80 * 1024);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    configured = true;
-  }
+  static DeviceOnce once;
+  once.run([&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
   launch_pdl(kern, grid, dim3(kTc2Threads), smem, s, g);
 }
 

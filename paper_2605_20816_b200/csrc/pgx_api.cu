@@ -74,6 +74,10 @@ struct pgx_problem {
   pgx_stats* d_stats = nullptr;   // host-mode staging
   long long* d_labels_out = nullptr;
   float* d_margin_out = nullptr;
+  // true between the first launch of a call and its tail launch: a call that
+  // failed in between leaves the fix-up / ticket counters armed, and the next
+  // call re-zeroes them first (normally the tail's last CTA re-arms them)
+  bool counters_dirty = false;
   int blocks1 = 0;   // general pass-1 blocks
   int splits = 1;    // pass-2 point splits
   GridPlan grid;     // regular-grid fast path plan (grid.enabled)
@@ -275,6 +279,15 @@ size_t workspace_estimate(const pgx_desc* d, int sms) {
 
 }  // namespace
 
+// counters a failed call may have left armed (see pgx_problem::counters_dirty)
+static pgx_status rearm_counters(pgx_problem* pb) {
+  if (!pb->counters_dirty) return PGX_OK;
+  PGX_CUDA(cudaMemsetAsync(pb->d_counters, 0, 4 * sizeof(int), pb->stream));
+  PGX_CUDA(cudaMemsetAsync(pb->d_fix_correct, 0, 2 * sizeof(long long), pb->stream));
+  pb->counters_dirty = false;
+  return PGX_OK;
+}
+
 // ====================================================================== ABI
 extern "C" {
 
@@ -393,7 +406,7 @@ pgx_status pgx_problem_create(const pgx_desc* desc, pgx_problem** out) {
       if (v < 0 || v >= pb->N) {
         pb->release();
         delete pb;
-        return fail(PGX_ERR_INVALID_ARGUMENT, "labels must lie in 1..%d", pb->N);
+        return fail(PGX_ERR_INVALID_ARGUMENT, "labels0 must lie in [0, %d)", pb->N);
       }
       l32[(size_t)q] = (int32_t)v;
     }
@@ -424,6 +437,11 @@ pgx_status pgx_set_stream(pgx_problem* pb, void* stream) {
 }
 
 int pgx_last_launch_count(pgx_problem* pb) { return pb ? pb->last_launches : 0; }
+
+int pgx_problem_path(pgx_problem* pb) {
+  if (!pb || !pb->grid.enabled) return PGX_PATH_GENERAL;
+  return pb->grid.tc ? PGX_PATH_GRID_TC : PGX_PATH_GRID_FP64;
+}
 
 pgx_status pgx_set_profiling(pgx_problem* pb, int enable) {
   if (!pb) return fail(PGX_ERR_INVALID_ARGUMENT, "problem must not be NULL");
@@ -457,9 +475,23 @@ pgx_status pgx_synchronize(pgx_problem* pb) {
   return PGX_OK;
 }
 
+static pgx_status eval_impl(pgx_problem* pb, const void* theta, double eps, double lambda,
+                            uint32_t flags, double* grad_out, pgx_stats* stats_out, bool force_general);
+
 pgx_status pgx_eval(pgx_problem* pb, const void* theta, double eps, double lambda, uint32_t flags,
                     double* grad_out, pgx_stats* stats_out) {
   g_last_error.clear();
+  pgx_status st = eval_impl(pb, theta, eps, lambda, flags, grad_out, stats_out, false);
+  if (st == PGX_OK && !(flags & PGX_DEVICE_PTRS) && (stats_out->flags & PGX_STAT_RANGE))
+    st = eval_impl(pb, theta, eps, lambda, flags, grad_out, stats_out, true);
+  else if (st == PGX_ERR_NUMERICAL && !(flags & PGX_DEVICE_PTRS) && pb->grid.enabled &&
+           (stats_out->flags & PGX_STAT_RANGE))
+    st = eval_impl(pb, theta, eps, lambda, flags, grad_out, stats_out, true);
+  return st;
+}
+
+static pgx_status eval_impl(pgx_problem* pb, const void* theta, double eps, double lambda,
+                            uint32_t flags, double* grad_out, pgx_stats* stats_out, bool force_general) {
   if (!pb) return fail(PGX_ERR_INVALID_ARGUMENT, "problem must not be NULL");
   if (!(eps > 0.0) || !std::isfinite(eps)) return fail(PGX_ERR_INVALID_ARGUMENT, "eps must be positive");
   if (!(lambda >= 0.0) || !std::isfinite(lambda))
@@ -475,9 +507,14 @@ pgx_status pgx_eval(pgx_problem* pb, const void* theta, double eps, double lambd
   cudaStream_t s = pb->stream;
   int launches = 0;
   pb->prof_reset();
+  if (rearm_counters(pb) != PGX_OK) return PGX_ERR_CUDA;
   const double* theta64 = nullptr;
   const float* theta32 = nullptr;
-  const bool fuse32 = pb->grid.enabled && pb->grid.tc && (flags & PGX_THETA_F32);
+  // fast modes check the logit-range bound of pgx.h PGX_STAT_RANGE on the
+  // device (tail kernel); with host buffers an out-of-range theta is then
+  // re-evaluated on the exact kernels (the general path) before returning
+  const bool use_grid = pb->grid.enabled && !force_general;
+  const bool fuse32 = use_grid && pb->grid.tc && (flags & PGX_THETA_F32);
   pgx_status st = stage_theta(pb, theta, flags, &theta64, &launches, fuse32 ? &theta32 : nullptr);
   if (st != PGX_OK) return st;
 
@@ -503,8 +540,8 @@ pgx_status pgx_eval(pgx_problem* pb, const void* theta, double eps, double lambd
     }
   }
   int blocks1 = pb->blocks1;
-
-  if (pb->grid.enabled) {
+  pb->counters_dirty = true;  // until the tail (which re-arms them) is enqueued
+  if (use_grid) {
     GridProf prof{pb, [](void* c, const char* n) { static_cast<pgx_problem*>(c)->prof_begin(n); },
                   [](void* c) { static_cast<pgx_problem*>(c)->prof_end(); }};
     st = grid_eval(pb->grid, prm, pb->prec, want_grad, s, &launches, &blocks1, prof);
@@ -526,18 +563,20 @@ pgx_status pgx_eval(pgx_problem* pb, const void* theta, double eps, double lambd
   }
   TailParams tp{};
   tp.want_grad = want_grad;
-  tp.fix_amb = pb->grid.enabled ? 1 : 0;
+  tp.fix_amb = use_grid ? 1 : 0;
   tp.ticket = reinterpret_cast<unsigned*>(pb->d_counters + 2);
   tp.part_th2 = pb->d_part_th2;
+  tp.range_c = use_grid ? 1.4426950408889634074 / eps : 0.0;
+  tp.range_bits = reinterpret_cast<unsigned*>(pb->d_counters + 3);
   ReduceParams& rp = tp.red;
   rp.K = pb->K;
   rp.N = pb->N;
-  rp.splits = pb->grid.enabled ? pb->grid.splits_out : pb->splits;
+  rp.splits = use_grid ? pb->grid.splits_out : pb->splits;
   rp.P = pb->P;
   rp.eps = eps;
   rp.lambda = lambda;
   rp.theta = theta64;
-  rp.part_g = pb->grid.enabled ? pb->grid.part_out : pb->d_part_g;
+  rp.part_g = use_grid ? pb->grid.part_out : pb->d_part_g;
   rp.grad_out = grad_dst;
   rp.nonfinite = pb->d_counters + 1;
   FinalParams& fp = tp.fin;
@@ -561,6 +600,7 @@ pgx_status pgx_eval(pgx_problem* pb, const void* theta, double eps, double lambd
   PGX_DISPATCH(launch_tail, prm, tp, tail_blocks, s);
   pb->prof_end();
   PGX_LAUNCH_CHECK();
+  pb->counters_dirty = false;
   ++launches;
   pb->last_launches = launches;
 
@@ -588,9 +628,11 @@ pgx_status pgx_assign(pgx_problem* pb, const void* theta, uint32_t flags, int64_
   PGX_CUDA(cudaSetDevice(pb->device));
   cudaStream_t s = pb->stream;
   int launches = 0;
+  if (rearm_counters(pb) != PGX_OK) return PGX_ERR_CUDA;
   const double* theta64 = nullptr;
   pgx_status st = stage_theta(pb, theta, flags, &theta64, &launches);
   if (st != PGX_OK) return st;
+  pb->counters_dirty = true;
   EvalParams prm = make_params(pb, 1.0);
   prm.theta = theta64;
   prm.labels_out = reinterpret_cast<long long*>(dev ? labels_out : (int64_t*)pb->d_labels_out);
@@ -616,6 +658,7 @@ pgx_status pgx_assign(pgx_problem* pb, const void* theta, uint32_t flags, int64_
   fp.stats_out = (stats_out && dev) ? (void*)stats_out : (void*)pb->d_stats;
   PGX_DISPATCH(launch_tail, prm, tp, pb->sms, s);
   PGX_LAUNCH_CHECK();
+  pb->counters_dirty = false;
   ++launches;
   pb->last_launches = launches;
   if (!dev) {

@@ -20,6 +20,7 @@
 
 #include <math_constants.h>
 
+#include "../../include/pgx.h"
 #include "pgx_common.cuh"
 
 namespace pgx {
@@ -387,7 +388,7 @@ struct FinalParams {
 
 struct StatsDev {
   double phi, err, e0, n_rescanned;
-  long long n_points, n_correct, n_ambiguous, n_nonfinite;
+  long long n_points, n_correct, n_ambiguous, n_nonfinite, flags;
 };
 
 static __global__ void __launch_bounds__(256) k_finalize(FinalParams prm) {
@@ -427,6 +428,7 @@ static __global__ void __launch_bounds__(256) k_finalize(FinalParams prm) {
     out->n_correct = cor;
     out->n_ambiguous = amb;
     out->n_nonfinite = nf + (isfinite(phi) ? 0 : 1);
+    out->flags = 0;
   }
 }
 
@@ -444,6 +446,11 @@ struct TailParams {
   int fix_amb;  // the re-scan decides the ambiguity of queued points (grid path)
   unsigned* ticket;
   double* part_th2;  // [gridDim.x] per-CTA partials of ||theta[:, :N-1]||^2
+  // fast modes: c = log2(e) / eps (0 = no check); the largest column L1 norm
+  // of theta (fp32 bits, atomicMax: order-independent) times c beyond
+  // PGX_FAST_RANGE sets PGX_STAT_RANGE
+  double range_c;
+  unsigned* range_bits;
 };
 
 constexpr int kTailThreads = 256;
@@ -565,6 +572,19 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(EvalParams e, TailParams 
     }
   }
 
+  // (1b) the logit-range bound of the fast modes (pgx.h PGX_STAT_RANGE)
+  if (t.range_c > 0.0) {
+    float vmax = 0.0f;
+    for (int i = blockIdx.x * kTailThreads + tid; i < t.fin.N; i += gridDim.x * kTailThreads) {
+      double a = 0.0;
+      for (int k = 0; k < t.fin.K; ++k) a += fabs(t.fin.theta[(int64_t)k * t.fin.N + i]);
+      vmax = fmaxf(vmax, a <= 3e38 ? (float)a : CUDART_INF_F);  // NaN -> inf
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, off));
+    if (lane == 0 && vmax > 0.0f) atomicMax(t.range_bits, __float_as_uint(vmax));
+  }
+
   // (3) last CTA: scalars
   __threadfence();
   __syncthreads();
@@ -611,6 +631,13 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(EvalParams e, TailParams 
     out->n_correct = cor;
     out->n_ambiguous = amb;
     out->n_nonfinite = nf + (isfinite(phi) ? 0 : 1);
+    long long flags = 0;
+    if (t.range_c > 0.0) {
+      const float rb = __uint_as_float(*(volatile unsigned*)t.range_bits);
+      if (!((double)rb * t.range_c <= PGX_FAST_RANGE)) flags |= PGX_STAT_RANGE;
+      *t.range_bits = 0u;
+    }
+    out->flags = flags;
     // re-arm the counters for the next call (stream-ordered)
     *e.fix_count = 0;
     *(long long*)prm.fix_correct = 0;

@@ -20,6 +20,7 @@ struct GridPlan {
   int dim = 2, D = 1;
   int R = 1, segs = 1, lines = 0, blocks1 = 0;
   int tc_blocks = 0;
+  bool sweep = false;  // pass 1 = k_tc_sweep (pgx_tc_sweep.cuh) instead of k_tc_pass1
   int tc2_gtiles = 0, tc2_lps = 1, tc2_splits = 0;  // tensor-core pass 2 (0 = CUDA-core pass 2)
   int64_t tc2_ips = 1;                               // its items per CTA row
   int part_splits = 0;                             // allocated split slots of part_g
@@ -40,20 +41,6 @@ struct GridPlan {
   double* pix_w = nullptr;
   float* pix_q = nullptr;
   int smem2 = 0;
-  // tc: the evaluation in line chunks so that pass 2 of chunk c (stream aux)
-  // runs while pass 1 of chunk c + 1 (the problem's stream) does: one CTA of
-  // each kernel per SM, whose latency-bound phases interleave
-  static constexpr int kMaxChunks = 8;
-  int tc_chunks = 1;
-  int64_t ch_tile[kMaxChunks + 1] = {};  // pass-1 tile range of chunk c: [ch_tile[c], ch_tile[c+1])
-  int ch_p1grid[kMaxChunks] = {};
-  int ch_part[kMaxChunks + 1] = {};      // pass-1 partial slots
-  int64_t ch_line[kMaxChunks + 1] = {};  // pass-2 line range
-  int ch_lps[kMaxChunks] = {}, ch_splits[kMaxChunks] = {};
-  int ch_split[kMaxChunks + 1] = {};     // pass-2 split slots
-  cudaStream_t aux = nullptr;
-  cudaEvent_t ev_p1[kMaxChunks] = {};
-  cudaEvent_t ev_join = nullptr;
 };
 
 // pass-2 line splits over `lines` lines: minimise waves x (lines per CTA + 1)
@@ -117,12 +104,16 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
   gp.blocks1 = gp.lines * gp.segs;
   // tensor-core pass 1: <= 2 CTAs per SM (256 TMEM columns each); R tiles of
   // 128 pixels share each chunk's coefficient build
-  gp.tc = d->precision == PGX_PREC_TC;
+  // (k_tc_coeffs puts the 128-grain chunks on gridDim.y)
+  gp.tc = d->precision == PGX_PREC_TC && (d->n_grains + 127) / 128 <= 65535;
   if (gp.tc) {
     // tensor-core pass 1: persistent, kT1CtasPerSm CTAs per SM, items of kT1Slots tiles
     const int64_t ntiles = (int64_t)gp.lines * (side / kTcThreadsTile);
     const int64_t items = (ntiles + kT1Slots - 1) / kT1Slots;
     gp.tc_blocks = (int)std::min<int64_t>(items, (int64_t)kT1CtasPerSm * sms);
+    const char* sw = getenv("PGX_TC_SWEEP");
+    gp.sweep = !(sw && sw[0] == '0');
+    if (gp.sweep) gp.tc_blocks = (int)std::min<int64_t>((ntiles + 3) / 4, (int64_t)sms);
     gp.blocks1 = gp.tc_blocks;
   }
   const int N = d->n_grains;
@@ -169,32 +160,6 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
       gp.tc2_splits = isp;
     }
     gp.splits_out = gp.tc2_splits;
-    // line chunks (>= 64 lines each): pass 1 one CTA per SM, pass 2 sized for
-    // the other half of each SM
-    const int tpl = side / kTcThreadsTile;
-    // (measured: c5 4 chunks 20.1 ms vs 17.3 ms unchunked -- each kernel at one
-    // CTA per SM loses more than the interleaving gains; off unless requested)
-    const char* env = getenv("PGX_TC_CHUNKS");
-    int C = env ? atoi(env) : 1;
-    C = std::max(1, std::min({C, GridPlan::kMaxChunks, gp.lines / 64}));
-    gp.tc_chunks = C;
-    if (C > 1) {
-      gp.ch_part[0] = 0;
-      gp.ch_split[0] = 0;
-      for (int c = 0; c <= C; ++c) gp.ch_line[c] = (int64_t)gp.lines * c / C;
-      for (int c = 0; c < C; ++c) {
-        const int nl = (int)(gp.ch_line[c + 1] - gp.ch_line[c]);
-        gp.ch_tile[c] = gp.ch_line[c] * tpl;
-        const int64_t items = ((int64_t)nl * tpl + kT1Slots - 1) / kT1Slots;
-        gp.ch_p1grid[c] = (int)std::min<int64_t>(items, sms);
-        gp.ch_part[c + 1] = gp.ch_part[c] + gp.ch_p1grid[c];
-        tc2_splits_for(nl, gp.tc2_gtiles, (int64_t)sms, 8 * sms, gp.ch_lps[c], gp.ch_splits[c]);
-        gp.ch_split[c + 1] = gp.ch_split[c] + gp.ch_splits[c];
-      }
-      gp.ch_tile[C] = (int64_t)gp.lines * tpl;
-      gp.blocks1 = gp.ch_part[C];
-      gp.splits_out = gp.ch_split[C];
-    }
     gp.part_splits = std::max(gp.splits, gp.splits_out);
   }
 }
@@ -244,28 +209,12 @@ inline cudaError_t grid_plan_create(GridPlan& gp, const pgx_desc* d, int sms, si
       gp.tc_pix = static_cast<unsigned char*>(gp.d_tc_pix);
       gp.tc_pix_ready = false;
     }
-    if (gp.tc_chunks > 1) {
-      e = cudaStreamCreateWithFlags(&gp.aux, cudaStreamNonBlocking);
-      if (e != cudaSuccess) return e;
-      for (int c = 0; c < gp.tc_chunks; ++c)
-        if ((e = cudaEventCreateWithFlags(&gp.ev_p1[c], cudaEventDisableTiming)) != cudaSuccess) return e;
-      if ((e = cudaEventCreateWithFlags(&gp.ev_join, cudaEventDisableTiming)) != cudaSuccess) return e;
-    }
   }
   return cudaSuccess;
 }
 
-inline void grid_plan_destroy(GridPlan& gp) {
-  for (cudaEvent_t& ev : gp.ev_p1)
-    if (ev) cudaEventDestroy(ev), ev = nullptr;
-  if (gp.ev_join) cudaEventDestroy(gp.ev_join), gp.ev_join = nullptr;
-  if (gp.aux) cudaStreamDestroy(gp.aux), gp.aux = nullptr;
-}
+inline void grid_plan_destroy(GridPlan& gp) { (void)gp; }
 
 }  // namespace pgx
 
 #include "pgx_launch.cuh"
-
-namespace pgx {
-
-}  // namespace pgx

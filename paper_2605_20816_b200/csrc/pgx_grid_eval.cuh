@@ -96,48 +96,16 @@ inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool wa
     }
     prof.end(prof.ctx);
     ++*launches;
-    if (gp.tc_chunks > 1) {
-      // line chunks: pass 1 of chunk c on s, pass 2 of chunk c on the aux
-      // stream once that pass 1 is done, overlapping pass 1 of chunk c + 1
-      prof.begin(prof.ctx, want_grad ? "tc_pass1+2" : "tc_pass1");
-      for (int c = 0; c < gp.tc_chunks; ++c) {
-        GridParams g1 = g;
-        g1.tile_lo = gp.ch_tile[c];
-        g1.tile_hi = gp.ch_tile[c + 1];
-        g1.part_off = gp.ch_part[c];
-        if (gp.dim == 2) {
-          PGX_GRID_DEG(2, tc_dispatch_pass1, g1, gp.ch_p1grid[c], s)
-        } else {
-          PGX_GRID_DEG3(tc_dispatch_pass1, g1, gp.ch_p1grid[c], s)
-        }
-        ++*launches;
-        if (!want_grad) continue;
-        if (cudaEventRecord(gp.ev_p1[c], s) != cudaSuccess) return PGX_ERR_CUDA;
-        if (cudaStreamWaitEvent(gp.aux, gp.ev_p1[c], 0) != cudaSuccess) return PGX_ERR_CUDA;
-        GridParams g2 = g;
-        g2.line_lo = gp.ch_line[c];
-        g2.lines = (int)gp.ch_line[c + 1];
-        g2.lines_per_split = gp.ch_lps[c];
-        g2.items_per_split = (int64_t)gp.ch_lps[c] * (g.side / kTc2Px);
-        g2.split_off = gp.ch_split[c];
-        dim3 grid(gp.tc2_gtiles, gp.ch_splits[c]);
-        if (gp.dim == 2) {
-          PGX_GRID_DEG(2, tc_dispatch_pass2, g2, grid, gp.aux)
-        } else {
-          PGX_GRID_DEG3(tc_dispatch_pass2, g2, grid, gp.aux)
-        }
-        ++*launches;
-      }
-      if (want_grad) {
-        if (cudaEventRecord(gp.ev_join, gp.aux) != cudaSuccess) return PGX_ERR_CUDA;
-        if (cudaStreamWaitEvent(s, gp.ev_join, 0) != cudaSuccess) return PGX_ERR_CUDA;
-      }
-      prof.end(prof.ctx);
-      *blocks1 = gp.blocks1;
-      return cudaPeekAtLastError() != cudaSuccess ? PGX_ERR_CUDA : PGX_OK;
-    }
+    // a failed table launch must not leave pass 1 reading stale images
+    if (cudaPeekAtLastError() != cudaSuccess) return PGX_ERR_CUDA;
     prof.begin(prof.ctx, "tc_pass1");
-    if (gp.dim == 2) {
+    if (gp.sweep) {
+      if (gp.dim == 2) {
+        PGX_GRID_DEG(2, tc_dispatch_sweep, g, gp.tc_blocks, s)
+      } else {
+        PGX_GRID_DEG3(tc_dispatch_sweep, g, gp.tc_blocks, s)
+      }
+    } else if (gp.dim == 2) {
       PGX_GRID_DEG(2, tc_dispatch_pass1, g, gp.tc_blocks, s)
     } else {
       PGX_GRID_DEG3(tc_dispatch_pass1, g, gp.tc_blocks, s)

@@ -6,6 +6,8 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <cstdint>
 #include <cstdlib>
 #include <utility>
 
@@ -24,6 +26,26 @@ inline bool pdl_enabled() {
   }();
   return on;
 }
+
+// A per-device one-time action (a kernel's cudaFuncSetAttribute applies to the
+// current device only): runs `f` the first time it is called on each device
+// ordinal; thread-safe (a racing duplicate call is harmless: the attribute
+// set is idempotent).
+struct DeviceOnce {
+  std::atomic<uint64_t> done{0};
+  template <typename F>
+  void run(F&& f) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      (void)cudaGetLastError();
+      dev = 0;
+    }
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    f();
+    done.fetch_or(bit, std::memory_order_acq_rel);
+  }
+};
 
 // launch `kern` with programmatic stream serialization (the kernel must call
 // griddep_wait() before touching its predecessor's data, see pgx_common.cuh)
@@ -68,6 +90,8 @@ template <int DIM, int D>
 void tc_dispatch_pix(const GridParams& g, const GridPlan& gp, cudaStream_t s);
 template <int DIM, int D>
 void tc_dispatch_pass1(const GridParams& g, int blocks, cudaStream_t s);
+template <int DIM, int D>
+void tc_dispatch_sweep(const GridParams& g, int blocks, cudaStream_t s);
 template <int DIM, int D>
 void tc_dispatch_pass2(const GridParams& g, dim3 grid, cudaStream_t s);
 

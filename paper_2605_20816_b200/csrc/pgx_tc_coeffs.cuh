@@ -41,8 +41,9 @@ __global__ void __launch_bounds__(kTcCoefChunk) k_tc_coeffs(GridParams g, double
   __shared__ double lc[K];
   __shared__ unsigned s_max, s_b1;
   const int tid = threadIdx.x;
-  const int chunk = blockIdx.x;
-  const int64_t line = blockIdx.y;
+  // lines on gridDim.x (3-D grids have side^2 > 65535 of them), chunks on y
+  const int chunk = blockIdx.y;
+  const int64_t line = blockIdx.x;
   const int i = chunk * kTcCoefChunk + tid;
   if (tid == 0) {
     double lcr[K];

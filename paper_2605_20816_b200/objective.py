@@ -46,6 +46,7 @@ class EvalStats(NamedTuple):
     n_ambiguous: int
     n_nonfinite: int
     n_rescanned: int = 0
+    flags: int = 0
 
 
 def _basis_key(basis):
@@ -148,14 +149,9 @@ class Problem:
 
     # fp32 / fp16-split logits carry ~2^-22 relative error; beyond this bound
     # on |h''| = |theta^T eta| / (eps ln 2) the error would reach 2^-6 in the
-    # exponent and the fast modes hand the call to the exact kernels
-    FAST_RANGE = 2.0 ** 16
-
-    def _fast_ok(self, t: np.ndarray, eps: float) -> bool:
-        if self.precision not in ("fp64", "tc"):
-            return True
-        bound = float(np.abs(t).sum(axis=0).max()) / (float(eps) * math.log(2.0))
-        return bound <= self.FAST_RANGE  # NaN/inf: False -> the exact path reports them
+    # exponent: the library then flags the result (pgx.h PGX_STAT_RANGE) and,
+    # for host buffers, re-evaluates it on the exact kernels itself
+    FAST_RANGE = _lib.PGX_FAST_RANGE
 
     def _exact_problem(self) -> "Problem":
         if self._exact is None:
@@ -172,6 +168,21 @@ class Problem:
 
     def set_stream(self, stream: int):
         _lib.check(self._lib.pgx_set_stream(self._h, stream))
+
+    @property
+    def kernel_path(self) -> str:
+        """'general', 'grid_fp64' or 'grid_tc' (pgx_problem_path)."""
+        return _lib.PATH_NAMES[int(self._lib.pgx_problem_path(self._h))]
+
+    def eval_kernels(self, theta, eps: float, **kw):
+        """eval() with kernel-level profiling: (result, stats, [kernel names])."""
+        self.set_profiling(True)
+        try:
+            res, st = self.eval(theta, eps, **kw)
+            names = [n for n, _ in self.profile()]
+        finally:
+            self.set_profiling(False)
+        return res, st, names
 
     def last_launch_count(self) -> int:
         return int(self._lib.pgx_last_launch_count(self._h))
@@ -201,9 +212,6 @@ class Problem:
              want_assign: bool = False) -> tuple[EvalResult, EvalStats]:
         """One fused evaluation with host buffers (copies inside the call)."""
         t, tflag = self._theta(theta)
-        if not self._fast_ok(t, eps):
-            return self._exact_problem().eval(theta, eps, lam=lam, want_grad=want_grad,
-                                              want_assign=want_assign)
         flags = tflag | (_lib.PGX_WANT_GRAD if want_grad else 0) | (
             _lib.PGX_WANT_ASSIGN if want_assign else 0)
         grad = np.empty((self.K, self.n_grains)) if want_grad else None
@@ -212,7 +220,7 @@ class Problem:
             _lib.check(self._lib.pgx_eval(self._h, t.ctypes.data, float(eps), float(lam), flags,
                                           _lib.as_ptr(grad), ctypes.addressof(st)))
             stats = EvalStats(st.phi, st.err, st.e0, st.n_points, st.n_correct, st.n_ambiguous,
-                              st.n_nonfinite, int(st.n_rescanned))
+                              st.n_nonfinite, int(st.n_rescanned), int(st.flags))
         res = EvalResult(phi=stats.phi, grad=grad,
                          err=stats.err if want_assign else None,
                          e0=stats.e0 if want_assign else None)
@@ -226,9 +234,7 @@ class Problem:
 
     def assign(self, theta, *, with_margin: bool = False):
         """Tie-tolerant hard assignment (1-based labels) without the N x P costs."""
-        t, tflag = self._theta(theta)
-        if not self._fast_ok(t, 1.0):  # (the arg-min does not depend on eps)
-            return self._exact_problem().assign(theta, with_margin=with_margin)
+        t, tflag = self._theta(theta)  # (pgx_assign always runs the exact fp64 kernels)
         labels = np.empty(self.n_points, dtype=np.int64)
         margin = np.empty(self.n_points, dtype=np.float32) if with_margin else None
         with self._lock:

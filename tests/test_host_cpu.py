@@ -49,7 +49,8 @@ def test_ctypes_signatures_cover_header(lib_path):
 
     assert set(header_functions()) == set(_lib.SIGNATURES)
     lib = _lib.load()
-    assert lib.pgx_abi_version() == 1
+    assert lib.pgx_abi_version() == _lib.ABI_VERSION
+    assert ctypes.sizeof(_lib.PgxStats) == 8 * _lib.STATS_WORDS
 
 
 def test_invalid_descriptors_rejected_without_gpu(lib_path):
