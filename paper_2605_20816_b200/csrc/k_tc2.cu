@@ -1,5 +1,6 @@
 // k_tc2.cu — tensor-core pass 2 and the per-evaluation operand tables; launchers declared in pgx_launch.cuh.
 #include "pgx_grid.cuh"
+#include "pgx_tc_grad.cuh"
 #include "pgx_launch.cuh"
 
 namespace pgx {
@@ -35,7 +36,18 @@ void tc_dispatch_pass2(const GridParams& g, dim3 grid, cudaStream_t s) {
     tc_launch_pass2<DIM, D, false>(g, grid, s);
 }
 
+template <int DIM, int D>
+void tc_dispatch_grad(const GridParams& g, dim3 grid, cudaStream_t s) {
+  auto kern = k_tc_grad<DIM, D>;
+  // padded so that <= 2 CTAs (2 x 256 TMEM columns) share an SM
+  const int smem = std::max(GdSmem<DIM, D>::TOTAL, 80 * 1024);
+  static DeviceOnce once;
+  once.run([&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
+  launch_pdl(kern, grid, dim3(kGdThreads), smem, s, g);
+}
+
 #define PGX_I(DIM, D) \
+  template void tc_dispatch_grad<DIM, D>(const GridParams&, dim3, cudaStream_t); \
   template void tc_dispatch_coeffs<DIM, D>(const GridParams&, const GridPlan&, cudaStream_t); \
   template void tc_dispatch_pix<DIM, D>(const GridParams&, const GridPlan&, cudaStream_t); \
   template void tc_dispatch_pass2<DIM, D>(const GridParams&, dim3, cudaStream_t);

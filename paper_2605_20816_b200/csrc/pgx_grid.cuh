@@ -21,6 +21,7 @@ struct GridPlan {
   int R = 1, segs = 1, lines = 0, blocks1 = 0;
   int tc_blocks = 0;
   bool sweep = false;  // pass 1 = k_tc_sweep (pgx_tc_sweep.cuh) instead of k_tc_pass1
+  bool grad = false;   // pass 2 = k_tc_grad (pgx_tc_grad.cuh) instead of k_tc_pass2
   int tc2_gtiles = 0, tc2_lps = 1, tc2_splits = 0;  // tensor-core pass 2 (0 = CUDA-core pass 2)
   int64_t tc2_ips = 1;                               // its items per CTA row
   int part_splits = 0;                             // allocated split slots of part_g
@@ -160,6 +161,8 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
       gp.tc2_splits = isp;
     }
     gp.splits_out = gp.tc2_splits;
+    const char* gd = getenv("PGX_TC_GRAD");
+    gp.grad = !(gd && gd[0] == '0');
     gp.part_splits = std::max(gp.splits, gp.splits_out);
   }
 }

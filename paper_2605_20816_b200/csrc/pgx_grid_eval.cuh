@@ -128,7 +128,13 @@ inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool wa
     g.items_per_split = gp.tc2_ips;
     g.splits = gp.tc2_splits;
     prof.begin(prof.ctx, "tc_pass2");
-    if (gp.dim == 2) {
+    if (gp.grad) {
+      if (gp.dim == 2) {
+        PGX_GRID_DEG(2, tc_dispatch_grad, g, grid, s)
+      } else {
+        PGX_GRID_DEG3(tc_dispatch_grad, g, grid, s)
+      }
+    } else if (gp.dim == 2) {
       PGX_GRID_DEG(2, tc_dispatch_pass2, g, grid, s)
     } else {
       PGX_GRID_DEG3(tc_dispatch_pass2, g, grid, s)

@@ -94,6 +94,8 @@ template <int DIM, int D>
 void tc_dispatch_sweep(const GridParams& g, int blocks, cudaStream_t s);
 template <int DIM, int D>
 void tc_dispatch_pass2(const GridParams& g, dim3 grid, cudaStream_t s);
+template <int DIM, int D>
+void tc_dispatch_grad(const GridParams& g, dim3 grid, cudaStream_t s);
 
 }  // namespace pgx
 

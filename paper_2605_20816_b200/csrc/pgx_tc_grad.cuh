@@ -1,0 +1,378 @@
+// pgx_tc_grad.cuh — PGX_PREC_TC pass 2 ("grad"): the gradient contraction
+// sum_x (onehot_G(x) - p(x)) eta(x) (objective.py:109-113) with both
+// contractions on the tensor cores (FlashAttention-backward-like, grain-major):
+//
+//   UMMA 1 (SS)  S^T[128 grains x 64 px] = B''(line)[grains x 3J] . L(x)[px x 3J]^T
+//   epilogue     thread = grain = TMEM lane: r' = p/2 * 2^13 = 2^(w13 - h~'')
+//                (packed FFMA2 argument pairs + MUFU.EX2), or -(1 - p_G)/2 * 2^13
+//                on the pixel's label grain (pass-1 record: no cancellation);
+//                split exactly into fp16 hi (the fp32 value with its 13 low
+//                mantissa bits cleared) + lo (the fp32 remainder) and written
+//                back into TMEM over S (packed f16x2)
+//   UMMA 2 (TS)  R[128 grains x 32] += r'_hi . [L_hi | L_lo]^T + r'_lo . [L_hi | L_lo]^T
+//                (A from TMEM, K = 16 pixels per MMA, 8 MMAs per tile)
+//
+// Warp specialisation, 320 threads, 2 CTAs per SM:
+//   warps 0-7  epilogue: warp w owns TMEM lanes 32 (w % 4) .. (grains) and the
+//              pixel half w / 4 of each 64-pixel tile;
+//   warp 8     MMA: one lane issues UMMA 2 of tile n and UMMA 1 of tile n + 3
+//              as soon as the epilogue of tile n has written r' (S is
+//              triple-buffered in TMEM) -- nothing else on its critical path;
+//   warp 9     loader: bulk copies (cp.async.bulk + mbarrier tx counts) of the
+//              line's coefficient image (kGdA slots) and each tile's pixel
+//              operands and pass-1 records (kGdBuf-deep), refilled as the
+//              MMAs reading them complete.
+// R alternates between two TMEM accumulators per group of 4 tiles; a finished
+// group is flushed into fp64 line sums 3 tiles later (when it is known to be
+// complete) and per line expanded into the K gradient rows of the CTA's split
+// slot of the partials (fp64; the tail reduces the splits in fixed order).
+//
+// TMEM (256 columns): S_0..S_2 [0, 192) (64 each), R_a [192, 224), R_b [224, 256).
+// Within S_s, pixel half h keeps r'_hi in [32h, 32h + 16) and r'_lo in
+// [32h + 16, 32h + 32): only columns its own warps have already read.
+#pragma once
+
+#include "pgx_grid_common.cuh"
+#include "pgx_tc_coeffs.cuh"
+#include "pgx_tc_common.cuh"
+#include "pgx_tc_pass2.cuh"  // kTc2* constants (the tile / record layout shared with pass 1)
+#include "pgx_tc_sweep.cuh"  // f32x2 helpers, mbar_spin
+
+namespace pgx {
+
+// pixel-operand + record buffers: the loader warp runs up to kGdBuf items
+// ahead of UMMA 2 (hides the L2 bulk-copy latency of several thousand cycles)
+constexpr int kGdBuf = 8;
+constexpr int kGdA = 3;    // coefficient-image slots (lines in flight)
+constexpr int kGdMmaWarp = kTc2Epi / 32, kGdLoadWarp = kGdMmaWarp + 1;
+constexpr int kGdThreads = kTc2Epi + 64;  // + MMA warp + loader warp
+
+template <int DIM, int D>
+struct GdSmem {
+  static constexpr int J = D + 1;
+  static constexpr int K = feature_count(DIM, D);
+  static constexpr int KS = tc_ksteps(J);
+  static constexpr int A1 = KS * kTc2Grains * 32;  // coefficient image (128 rows)
+  static constexpr int PIX = tc_pix_bytes<J>();
+  static constexpr int REC = kTc2RecFloats * 4;
+  static constexpr int A1_OFF = 0;
+  static constexpr int PIX_OFF = A1_OFF + kGdA * A1;
+  static constexpr int REC_OFF = PIX_OFF + kGdBuf * PIX;
+  static constexpr int R_OFF = REC_OFF + kGdBuf * REC;  // fp64 [J][128] line sums
+  static constexpr int TOTAL = R_OFF + J * kTc2Grains * 8;
+};
+
+// fp16 pair of two fp32 values, low half = a (the even pixel)
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
+
+// Once per line and grain: grad rows += line factors x the line's fp64 sums,
+// acc[k N] (the grain's column of its split slot) += lc[k] R_{alpha_fast(k)}.
+// Out of line so that its 16-deep load batches do not weigh on the register
+// allocation of the tile loop.
+template <int DIM, int D>
+__device__ __noinline__ void tc_grad_line(double* __restrict__ acc, int N, const double* __restrict__ lcp,
+                                          const double* R64, bool first) {
+  constexpr int K = feature_count(DIM, D);
+  constexpr int J = D + 1;
+  const double rs = -2.0 / (8192.0 * 1024.0);  // R_true = -2 R' 2^-(13 + 10): r' = -r
+  double r[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) r[j] = rs * R64[j * kTc2Grains];
+  constexpr int CH = 16;
+#pragma unroll
+  for (int k0 = 0; k0 < K; k0 += CH) {
+    double prev[CH];
+#pragma unroll
+    for (int k = k0; k < k0 + CH && k < K; ++k) prev[k - k0] = first ? 0.0 : acc[(int64_t)k * N];
+#pragma unroll
+    for (int k = k0; k < k0 + CH && k < K; ++k)
+      acc[(int64_t)k * N] = fma(__ldg(lcp + k), r[alpha_of(DIM, D, k, DIM - 1)], prev[k - k0]);
+  }
+}
+
+template <int DIM, int D>
+__global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
+  using L = GdSmem<DIM, D>;
+  constexpr int J = L::J;
+  constexpr int K = L::K;
+  constexpr int KS = L::KS;
+  constexpr uint32_t IDESC1 = umma_idesc_f16(128, kTc2Px);
+  constexpr uint32_t IDESC2 = umma_idesc_f16(128, 32);
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t bar_full[kGdBuf], bar_pf[kGdBuf], bar_a[kGdA], bar_af[kGdA];
+  __shared__ uint64_t bar_s[kTc2S], bar_p[kTc2S], bar_end;
+  __shared__ unsigned tmem_base;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gbase = blockIdx.x * kTc2Grains;
+  // items (line, tile) of this CTA: [a0, a1) of the launch's line range
+  const int ntiles = g.side / kTc2Px;
+  const int gpl = (ntiles + kTc2Group - 1) / kTc2Group;  // R groups per line
+  const int64_t a0 = g.line_lo * ntiles + (int64_t)blockIdx.y * g.items_per_split;
+  const int64_t a1 = min((int64_t)g.lines * ntiles, a0 + g.items_per_split);
+  if (a1 <= a0) return;
+  const int nitems = (int)(a1 - a0);
+  const int64_t l0 = a0 / ntiles;
+  const int t0 = (int)(a0 - l0 * ntiles);
+  const int nlines = (int)((a1 - 1) / ntiles - l0 + 1);
+
+  if (warp == kGdMmaWarp) tmem_alloc(&tmem_base, 256);
+  if (tid == kTc2Epi) {
+    for (int b = 0; b < kGdBuf; ++b) {
+      mbar_init(&bar_full[b], 1);
+      mbar_init(&bar_pf[b], 1);
+    }
+    for (int b = 0; b < kGdA; ++b) {
+      mbar_init(&bar_a[b], 1);
+      mbar_init(&bar_af[b], 1);
+    }
+    for (int b = 0; b < kTc2S; ++b) {
+      mbar_init(&bar_s[b], 1);
+      mbar_init(&bar_p[b], kTc2Epi / 32);
+    }
+    mbar_init(&bar_end, 1);
+    fence_mbar_init();
+  }
+  {  // zero the fp64 line sums
+    double* R = reinterpret_cast<double*>(smem + L::R_OFF);
+    for (int e = tid; e < J * kTc2Grains; e += kGdThreads) R[e] = 0.0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  griddep_wait();  // PDL: pass 1's records, fix lists and partials are complete
+  const unsigned tmem = tmem_base;
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
+  // the (line, tile) of an item, walked incrementally
+  struct Cur {
+    int n, li, t;
+    __device__ __forceinline__ void next(int nt) {
+      ++n;
+      if (++t == nt) {
+        t = 0;
+        ++li;
+      }
+    }
+  };
+  auto group_last = [&](const Cur& c) {
+    return c.t == ntiles - 1 || (c.t & (kTc2Group - 1)) == kTc2Group - 1 || c.n == nitems - 1;
+  };
+  auto r_col = [&](const Cur& c) {  // R accumulator of the item's group
+    return tmem + 192u + 32u * (unsigned)((c.li * gpl + c.t / kTc2Group) & 1);
+  };
+
+  if (warp == kGdLoadWarp) {
+    // ======================= loader warp: every image and every item's pixel
+    // operands + records, in consumption order; a buffer is refilled once the
+    // MMAs that read it are complete (commits of the MMA warp)
+    Cur cl{0, 0, t0};
+    int al = 0;  // lines whose coefficient image has been requested
+    for (; cl.n < nitems; cl.next(ntiles)) {
+      if (cl.n == 0 || cl.t == 0) {  // the line's image (lines ahead as the slots free up)
+        for (; al <= cl.li && al < nlines; ++al) {
+          const int ab = al % kGdA;
+          if (al >= kGdA) mbar_wait_sleep(&bar_af[ab], (unsigned)((al - kGdA) / kGdA) & 1u);
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&bar_a[ab], L::A1);
+            bulk_g2s(smem + L::A1_OFF + ab * L::A1,
+                     g.tc_img + ((l0 + al) * g.tc_nchunks + blockIdx.x) * (int64_t)L::A1, L::A1, &bar_a[ab]);
+          }
+          __syncwarp();
+        }
+      }
+      const int b = cl.n % kGdBuf;
+      if (cl.n >= kGdBuf) mbar_wait_sleep(&bar_pf[b], (unsigned)((cl.n - kGdBuf) / kGdBuf) & 1u);
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&bar_full[b], L::PIX + L::REC);
+        bulk_g2s(smem + L::PIX_OFF + b * L::PIX, g.tc_pix + (int64_t)cl.t * L::PIX, L::PIX, &bar_full[b]);
+        bulk_g2s(smem + L::REC_OFF + b * L::REC,
+                 g.tc_rec + ((l0 + cl.li) * ntiles + cl.t) * (int64_t)kTc2RecFloats, L::REC, &bar_full[b]);
+      }
+      __syncwarp();
+    }
+  } else if (warp == kGdMmaWarp) {
+    // ======================= MMA warp (warp-uniform loop, one lane issues)
+    const bool leader = lane == 0;
+    const uint64_t d_a1 = umma_desc(sbase + L::A1_OFF);
+    const uint64_t d_pix = umma_desc(sbase + L::PIX_OFF);
+    Cur cs{0, 0, t0}, cm{0, 0, t0};  // next UMMA 1, next UMMA 2
+    auto issue_s = [&]() {  // UMMA 1 of item cs into S_(n % 3)
+      const int b = cs.n % kGdBuf, st = cs.n % kTc2S, ab = cs.li % kGdA;
+      if (cs.t == 0 || cs.n == 0) mbar_wait(&bar_a[ab], (unsigned)(cs.li / kGdA) & 1u);
+      mbar_wait(&bar_full[b], (unsigned)(cs.n / kGdBuf) & 1u);
+      tc_fence_after();
+      if (leader) {
+        const uint64_t da = d_a1 + (uint64_t)((ab * L::A1) >> 4);
+        const uint64_t db = d_pix + (uint64_t)((b * L::PIX) >> 4);
+#pragma unroll
+        for (int s = 0; s < KS; ++s)
+          umma_f16_ss(tmem + 64u * st, da + (uint64_t)((s * kTc2Grains * 32) >> 4),
+                      db + (uint64_t)((s * kTc2Px * 32) >> 4), IDESC1, s > 0);
+        umma_commit(&bar_s[st]);
+        if (cs.t == ntiles - 1 || cs.n == nitems - 1) umma_commit(&bar_af[ab]);  // the line's image is free
+      }
+      __syncwarp();
+      cs.next(ntiles);
+    };
+    while (cs.n < nitems && cs.n < kTc2S) issue_s();
+    for (int k = 0; k < nitems; ++k) {
+      const int st = k % kTc2S, b = k % kGdBuf;
+      mbar_wait(&bar_p[st], (unsigned)(k / kTc2S) & 1u);  // r' of item k is in S_st
+      tc_fence_after();
+      if (leader) {  // UMMA 2: R += [r_hi; r_lo] . [L_hi | L_lo]^T over the 64 pixels
+        const unsigned tr = r_col(cm);
+        const unsigned ts = tmem + 64u * st;
+        const uint64_t dl = d_pix + (uint64_t)((b * L::PIX + KS * (kTc2Px * 32)) >> 4);
+        const bool fresh = (cm.t & (kTc2Group - 1)) == 0 || cm.n == 0;  // a group's first item
+#pragma unroll
+        for (int s = 0; s < 2 * (kTc2Px / 16); ++s) {
+          const int p = s / (kTc2Px / 16), ks = s % (kTc2Px / 16);
+          // pixels [16 ks, 16 ks + 16): half ks / 2, packed columns 8 (ks % 2); p = 1: r_lo
+          const unsigned a = ts + 32u * (ks >> 1) + 8u * (ks & 1) + (p == 1 ? 16u : 0u);
+          const uint64_t bo = dl + (uint64_t)((ks * 1024) >> 4);
+          umma_f16_ts(tr, a, bo, IDESC2, !(fresh && s == 0));
+        }
+        umma_commit(&bar_pf[b]);  // item k's pixel / record buffer is free once UMMA 2 is done
+        if (k == nitems - 1) umma_commit(&bar_end);
+      }
+      __syncwarp();
+      cm.next(ntiles);
+      if (cs.n < nitems) issue_s();  // item k + 3 into the S stage item k just released
+    }
+  } else {
+    // ======================= epilogue warps
+    const int q = warp & 3, h = warp >> 2;  // lane quarter, pixel half
+    const int i = gbase + 32 * q + lane;     // this thread's grain (TMEM lane)
+    const int g0w = gbase + 32 * q;          // the warp's first grain
+    const unsigned lane_off = (unsigned)(32 * q) << 16;
+    // this grain's fp64 line sums [J] in shared memory (stride 128:
+    // conflict-free, no registers held across the tile loop); its gradient rows
+    // [K] accumulate per line in the CTA's split slot of the partials
+    double* acc = g.part_g + (int64_t)(g.split_off + blockIdx.y) * K * g.N + (i < g.N ? i : 0);
+    double* R64 = reinterpret_cast<double*>(smem + L::R_OFF) + 32 * q + lane;
+    auto flush = [&](const Cur& c) {  // group of item c complete -> fp64; line -> K rows
+      uint32_t rv[16], rw[16];
+      tmem_ld16_nowait(r_col(c) + lane_off, rv);
+      tmem_ld16_nowait(r_col(c) + lane_off + 16u, rw);
+      tmem_ld_wait();
+      tmem_regs_ready(rv);
+      tmem_regs_ready(rw);
+#pragma unroll
+      for (int j = 0; j < J; ++j)
+        R64[j * kTc2Grains] += (double)__uint_as_float(rv[j]) + (double)__uint_as_float(rw[j]);
+      if (c.t == ntiles - 1 || c.n == nitems - 1) {  // the line's (or the CTA's) last item
+        if (i < g.N) tc_grad_line<DIM, D>(acc, g.N, g.tc_lc + (l0 + c.li) * K, R64, c.li == 0);
+#pragma unroll
+        for (int j = 0; j < J; ++j) R64[j * kTc2Grains] = 0.0;
+      }
+    };
+
+    const unsigned sbar_s = (unsigned)__cvta_generic_to_shared(&bar_s[0]);
+    const unsigned sbar_f = (unsigned)__cvta_generic_to_shared(&bar_full[0]);
+    int sB_next = g.tc_meta[l0 * g.tc_nchunks + blockIdx.x].x;
+    float inv = 0.0f;
+    int st = 0, b = 0;
+    unsigned ph_s = 0u, ph_f = 0u;  // phases of the S stage / buffer of the current item
+    Cur c{0, 0, t0}, cf{0, 0, t0};  // current item; item whose group may be flushed (lags by kTc2S)
+    for (; c.n < nitems; c.next(ntiles)) {
+      if (c.t == 0 || c.n == 0) {
+        inv = __int_as_float((127 - (sB_next + 10)) << 23);  // 2^-(sB + 10): S * inv = h~''
+        if (c.li + 1 < nlines) sB_next = g.tc_meta[(l0 + c.li + 1) * g.tc_nchunks + blockIdx.x].x;
+      }
+      const unsigned ts = tmem + 64u * st + lane_off + 32u * h;
+      const float* rec = reinterpret_cast<const float*>(smem + L::REC_OFF + b * L::REC) + 32 * h;
+      mbar_spin(sbar_s + 8u * st, ph_s);
+      tc_fence_after();
+      // UMMA 1 of this item follows UMMA 2 of item n - 3: that group may be final
+      if (c.n >= kTc2S) {
+        if (h == 0 && group_last(cf)) flush(cf);
+        cf.next(ntiles);
+      }
+      uint32_t sv[32];
+      tmem_ld32_nowait(ts, sv);
+      mbar_spin(sbar_f + 8u * b, ph_f);  // records visible
+      // label grains of this warp among the half-tile's pixels (rare)
+      const int lab_x = reinterpret_cast<const int*>(rec)[3 * kTc2Px + lane];
+      const unsigned hit = __ballot_sync(0xffffffffu, (unsigned)(lab_x - g0w) < 32u);
+      tmem_ld_wait();
+      tmem_regs_ready(sv);
+      const unsigned long long ninv2 = f2pack(-inv, -inv);
+      float rr[32];
+#ifdef PGX_GD_NOEPI
+#pragma unroll
+      for (int x = 0; x < 32; ++x) rr[x] = __uint_as_float(sv[x]) * inv;
+#else
+#pragma unroll
+      for (int x4 = 0; x4 < 32; x4 += 4) {
+        const float4 w4 = *reinterpret_cast<const float4*>(rec + x4);
+        const unsigned long long a01 =
+            ffma2(f2pack(__uint_as_float(sv[x4]), __uint_as_float(sv[x4 + 1])), ninv2, f2pack(w4.x, w4.y));
+        const unsigned long long a23 =
+            ffma2(f2pack(__uint_as_float(sv[x4 + 2]), __uint_as_float(sv[x4 + 3])), ninv2, f2pack(w4.z, w4.w));
+        rr[x4] = ex2_approx(f2lo(a01));  // p/2 * 2^13 = 2^(13 + w - h~'')
+        rr[x4 + 1] = ex2_approx(f2hi(a01));
+        rr[x4 + 2] = ex2_approx(f2lo(a23));
+        rr[x4 + 3] = ex2_approx(f2hi(a23));
+      }
+#endif
+      if (hit) {  // label grain: -(1 - p_G)/2 * 2^13 from pass 1 (no cancellation)
+        // the pixels of each distinct in-range label at once (a 32-pixel run
+        // mostly lies in one grain): one round per distinct label, not per pixel
+        const unsigned same = __match_any_sync(0xffffffffu, lab_x);
+        unsigned mine = 0u;
+        for (unsigned m = hit; m;) {
+          const int x = __ffs(m) - 1;
+          const unsigned grp = __shfl_sync(0xffffffffu, same, x);
+          if (__shfl_sync(0xffffffffu, lab_x, x) == i) mine = grp;
+          m &= ~grp;
+        }
+        if (__any_sync(0xffffffffu, mine != 0u)) {
+          const float* qn = rec + 2 * kTc2Px;
+#pragma unroll
+          for (int x = 0; x < 32; ++x)
+            if (mine & (1u << x)) rr[x] = qn[x];
+        }
+      }
+      // exact split: hi = rr with the 13 low mantissa bits cleared (an fp16
+      // value), lo = rr - hi (exact in fp32, |lo| < 2^-10 |rr|) rounded to fp16
+      uint32_t pp[32];  // [0, 16): r'_hi pairs, [16, 32): r'_lo pairs
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) {
+        const float h0 = __uint_as_float(__float_as_uint(rr[2 * cc]) & 0xffffe000u);
+        const float h1 = __uint_as_float(__float_as_uint(rr[2 * cc + 1]) & 0xffffe000u);
+        const unsigned long long lo2 =
+            ffma2(f2pack(h0, h1), f2pack(-1.0f, -1.0f), f2pack(rr[2 * cc], rr[2 * cc + 1]));
+        pp[cc] = pack_h2(h0, h1);
+        pp[16 + cc] = pack_h2(f2lo(lo2), f2hi(lo2));
+      }
+      tmem_st32(ts, pp);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_p[st]);
+      // next item's stage / buffer and phases
+      if (++st == kTc2S) {
+        st = 0;
+        ph_s ^= 1u;
+      }
+      if (++b == kGdBuf) {
+        b = 0;
+        ph_f ^= 1u;
+      }
+    }
+    // the last groups: complete once the final commit lands
+    mbar_wait(&bar_end, 0);
+    tc_fence_after();
+    for (; cf.n < nitems; cf.next(ntiles))
+      if (h == 0 && group_last(cf)) flush(cf);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kGdMmaWarp) tmem_dealloc(tmem, 256);
+}
+
+}  // namespace pgx

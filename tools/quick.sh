@@ -9,13 +9,14 @@ if [ -n "$K" ]; then
 fi
 for cb in $BENCHES; do
   cfg=${cb%%:*}; prec=${cb##*:}
-  timeout 300 python bench.py --config $cfg --precision $prec --no-cpu-baseline --steps 10 --warmup 3 > gpurun_out/q_${cfg}_${prec}.json 2> gpurun_out/q_${cfg}_${prec}.err
+  timeout 300 python bench.py --config $cfg --precision $prec --no-cpu-baseline --also "" --steps 10 --warmup 3 > gpurun_out/q_${cfg}_${prec}.json 2> gpurun_out/q_${cfg}_${prec}.err
   python - "$cfg" "$prec" <<'PY'
 import json, sys
 cfg, prec = sys.argv[1:3]
 try:
     d = json.loads(open(f"gpurun_out/q_{cfg}_{prec}.json").read().strip().splitlines()[-1])
-    print(cfg, prec, "ms/step %.4f e2e %.4f" % (d["ms_per_step"], d["e2e"]["ms_per_step"]), {k: round(v, 4) for k, v in d["roofline"]["kernels_ms"].items()} if "kernels_ms" in d["roofline"] else d["kernels_ms"], "binding", d["roofline"]["binding_pipe"], round(d["roofline"]["binding_frac"], 3), "phi", d["result"]["phi"])
+    r = d["roofline"]
+    print(cfg, prec, "ms/step %.4f e2e %.4f" % (d["ms_per_step"], d["e2e"]["ms_per_step"]), {k: round(v, 4) for k, v in r["kernels_ms"].items()}, "frac %.3f bound %s" % (r["frac"], r["bound"]), "phi", d["result"]["phi"])
 except Exception as e:
     print(cfg, prec, "FAILED", e); print(open(f"gpurun_out/q_{cfg}_{prec}.err").read()[-3000:])
 PY
