@@ -1,21 +1,12 @@
-// k_tc1.cu — tensor-core pass 1; launcher declared in pgx_launch.cuh.
+// k_tc1.cu — tensor-core pass 1 (pgx_tc_sweep.cuh); launcher declared in pgx_launch.cuh.
 #include "pgx_grid.cuh"
-#include "pgx_tc_sweep.cuh"
 #include "pgx_launch.cuh"
+#include "pgx_tc_sweep.cuh"
 
 namespace pgx {
 
 template <int DIM, int D>
 void tc_dispatch_pass1(const GridParams& g, int blocks, cudaStream_t s) {
-  auto kern = k_tc_pass1<DIM, D>;
-  const int smem = TcP1Smem<D + 1>::TOTAL;
-  static DeviceOnce once;
-  once.run([&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
-  launch_pdl(kern, dim3(blocks), dim3(kT1Threads), smem, s, g);
-}
-
-template <int DIM, int D>
-void tc_dispatch_sweep(const GridParams& g, int blocks, cudaStream_t s) {
   auto kern = k_tc_sweep<DIM, D>;
   const int smem = SwSmem<D + 1>::TOTAL;
   static DeviceOnce once;
@@ -23,9 +14,7 @@ void tc_dispatch_sweep(const GridParams& g, int blocks, cudaStream_t s) {
   launch_pdl(kern, dim3(blocks), dim3(kSwThreads), smem, s, g);
 }
 
-#define PGX_I(DIM, D)                                                                \
-  template void tc_dispatch_pass1<DIM, D>(const GridParams&, int, cudaStream_t); \
-  template void tc_dispatch_sweep<DIM, D>(const GridParams&, int, cudaStream_t);
+#define PGX_I(DIM, D) template void tc_dispatch_pass1<DIM, D>(const GridParams&, int, cudaStream_t);
 PGX_INST_GRID(PGX_I)
 
 }  // namespace pgx

@@ -1,4 +1,5 @@
-// k_tc2.cu — tensor-core pass 2 and the per-evaluation operand tables; launchers declared in pgx_launch.cuh.
+// k_tc2.cu — tensor-core pass 2 (pgx_tc_grad.cuh) and the per-evaluation operand
+// tables (pgx_tc_coeffs.cuh); launchers declared in pgx_launch.cuh.
 #include "pgx_grid.cuh"
 #include "pgx_tc_grad.cuh"
 #include "pgx_launch.cuh"
@@ -18,26 +19,8 @@ void tc_dispatch_pix(const GridParams& g, const GridPlan& gp, cudaStream_t s) {
   k_tc_pix<D><<<g.side / kTcPixTile, kTcPixTile, 0, s>>>(g.M, g.legendre, gp.tc_pix);
 }
 
-template <int DIM, int D, bool MID>
-void tc_launch_pass2(const GridParams& g, dim3 grid, cudaStream_t s) {
-  auto kern = k_tc_pass2<DIM, D, MID>;
-  // padded so that <= 2 CTAs (2 x 256 TMEM columns) share an SM
-  const int smem = std::max(TcP2Smem<D + 1>::TOTAL, 80 * 1024);
-  static DeviceOnce once;
-  once.run([&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
-  launch_pdl(kern, grid, dim3(kTc2Threads), smem, s, g);
-}
-
 template <int DIM, int D>
 void tc_dispatch_pass2(const GridParams& g, dim3 grid, cudaStream_t s) {
-  if (g.items_per_split % (g.side / kTc2Px) != 0)
-    tc_launch_pass2<DIM, D, true>(g, grid, s);  // CTA ranges start and end mid-line
-  else
-    tc_launch_pass2<DIM, D, false>(g, grid, s);
-}
-
-template <int DIM, int D>
-void tc_dispatch_grad(const GridParams& g, dim3 grid, cudaStream_t s) {
   auto kern = k_tc_grad<DIM, D>;
   // padded so that <= 2 CTAs (2 x 256 TMEM columns) share an SM
   const int smem = std::max(GdSmem<DIM, D>::TOTAL, 80 * 1024);
@@ -47,7 +30,6 @@ void tc_dispatch_grad(const GridParams& g, dim3 grid, cudaStream_t s) {
 }
 
 #define PGX_I(DIM, D) \
-  template void tc_dispatch_grad<DIM, D>(const GridParams&, dim3, cudaStream_t); \
   template void tc_dispatch_coeffs<DIM, D>(const GridParams&, const GridPlan&, cudaStream_t); \
   template void tc_dispatch_pix<DIM, D>(const GridParams&, const GridPlan&, cudaStream_t); \
   template void tc_dispatch_pass2<DIM, D>(const GridParams&, dim3, cudaStream_t);

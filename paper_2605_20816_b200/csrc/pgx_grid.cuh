@@ -9,8 +9,7 @@
 #include "pgx_grid_common.cuh"
 #include "pgx_grid_pass1.cuh"
 #include "pgx_grid_pass2.cuh"
-#include "pgx_tc_pass1.cuh"
-#include "pgx_tc_pass2.cuh"
+#include "pgx_tc_shared.cuh"
 
 namespace pgx {
 
@@ -20,8 +19,6 @@ struct GridPlan {
   int dim = 2, D = 1;
   int R = 1, segs = 1, lines = 0, blocks1 = 0;
   int tc_blocks = 0;
-  bool sweep = false;  // pass 1 = k_tc_sweep (pgx_tc_sweep.cuh) instead of k_tc_pass1
-  bool grad = false;   // pass 2 = k_tc_grad (pgx_tc_grad.cuh) instead of k_tc_pass2
   int tc2_gtiles = 0, tc2_lps = 1, tc2_splits = 0;  // tensor-core pass 2 (0 = CUDA-core pass 2)
   int64_t tc2_ips = 1;                               // its items per CTA row
   int part_splits = 0;                             // allocated split slots of part_g
@@ -108,13 +105,9 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
   // (k_tc_coeffs puts the 128-grain chunks on gridDim.y)
   gp.tc = d->precision == PGX_PREC_TC && (d->n_grains + 127) / 128 <= 65535;
   if (gp.tc) {
-    // tensor-core pass 1: persistent, kT1CtasPerSm CTAs per SM, items of kT1Slots tiles
+    // tensor-core pass 1 (k_tc_sweep): persistent, one CTA per SM, items of 4 tiles
     const int64_t ntiles = (int64_t)gp.lines * (side / kTcThreadsTile);
-    const int64_t items = (ntiles + kT1Slots - 1) / kT1Slots;
-    gp.tc_blocks = (int)std::min<int64_t>(items, (int64_t)kT1CtasPerSm * sms);
-    const char* sw = getenv("PGX_TC_SWEEP");
-    gp.sweep = !(sw && sw[0] == '0');
-    if (gp.sweep) gp.tc_blocks = (int)std::min<int64_t>((ntiles + 3) / 4, (int64_t)sms);
+    gp.tc_blocks = (int)std::min<int64_t>((ntiles + 3) / 4, (int64_t)sms);
     gp.blocks1 = gp.tc_blocks;
   }
   const int N = d->n_grains;
@@ -161,8 +154,6 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
       gp.tc2_splits = isp;
     }
     gp.splits_out = gp.tc2_splits;
-    const char* gd = getenv("PGX_TC_GRAD");
-    gp.grad = !(gd && gd[0] == '0');
     gp.part_splits = std::max(gp.splits, gp.splits_out);
   }
 }

@@ -99,13 +99,7 @@ inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool wa
     // a failed table launch must not leave pass 1 reading stale images
     if (cudaPeekAtLastError() != cudaSuccess) return PGX_ERR_CUDA;
     prof.begin(prof.ctx, "tc_pass1");
-    if (gp.sweep) {
-      if (gp.dim == 2) {
-        PGX_GRID_DEG(2, tc_dispatch_sweep, g, gp.tc_blocks, s)
-      } else {
-        PGX_GRID_DEG3(tc_dispatch_sweep, g, gp.tc_blocks, s)
-      }
-    } else if (gp.dim == 2) {
+    if (gp.dim == 2) {
       PGX_GRID_DEG(2, tc_dispatch_pass1, g, gp.tc_blocks, s)
     } else {
       PGX_GRID_DEG3(tc_dispatch_pass1, g, gp.tc_blocks, s)
@@ -128,13 +122,7 @@ inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool wa
     g.items_per_split = gp.tc2_ips;
     g.splits = gp.tc2_splits;
     prof.begin(prof.ctx, "tc_pass2");
-    if (gp.grad) {
-      if (gp.dim == 2) {
-        PGX_GRID_DEG(2, tc_dispatch_grad, g, grid, s)
-      } else {
-        PGX_GRID_DEG3(tc_dispatch_grad, g, grid, s)
-      }
-    } else if (gp.dim == 2) {
+    if (gp.dim == 2) {
       PGX_GRID_DEG(2, tc_dispatch_pass2, g, grid, s)
     } else {
       PGX_GRID_DEG3(tc_dispatch_pass2, g, grid, s)

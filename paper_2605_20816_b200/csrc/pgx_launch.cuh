@@ -83,7 +83,7 @@ void grid_dispatch_pass1(const GridParams& g, int R, int blocks, cudaStream_t s)
 template <int DIM, int D>
 void grid_dispatch_pass2(const GridParams& g, int GT, dim3 grid, int smem, cudaStream_t s);
 
-// tensor-core path: pgx_tc_coeffs.cuh, pgx_tc_pass1.cuh, pgx_tc_pass2.cuh
+// tensor-core path: pgx_tc_coeffs.cuh, pgx_tc_sweep.cuh (pass 1), pgx_tc_grad.cuh (pass 2)
 template <int DIM, int D>
 void tc_dispatch_coeffs(const GridParams& g, const GridPlan& gp, cudaStream_t s);
 template <int DIM, int D>
@@ -91,11 +91,7 @@ void tc_dispatch_pix(const GridParams& g, const GridPlan& gp, cudaStream_t s);
 template <int DIM, int D>
 void tc_dispatch_pass1(const GridParams& g, int blocks, cudaStream_t s);
 template <int DIM, int D>
-void tc_dispatch_sweep(const GridParams& g, int blocks, cudaStream_t s);
-template <int DIM, int D>
 void tc_dispatch_pass2(const GridParams& g, dim3 grid, cudaStream_t s);
-template <int DIM, int D>
-void tc_dispatch_grad(const GridParams& g, dim3 grid, cudaStream_t s);
 
 }  // namespace pgx
 

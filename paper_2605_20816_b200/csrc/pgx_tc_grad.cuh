@@ -13,8 +13,8 @@
 //                (A from TMEM, K = 16 pixels per MMA, 8 MMAs per tile)
 //
 // Warp specialisation, 320 threads, 2 CTAs per SM:
-//   warps 0-7  epilogue: warp w owns TMEM lanes 32 (w % 4) .. (grains) and the
-//              pixel half w / 4 of each 64-pixel tile;
+//   warps 0-7  epilogue: warp w owns TMEM lanes 32 (w % 4) .. (grains); warps
+//              0-3 take the even tiles, 4-7 the odd ones (all 64 pixels);
 //   warp 8     MMA: one lane issues UMMA 2 of tile n and UMMA 1 of tile n + 3
 //              as soon as the epilogue of tile n has written r' (S is
 //              triple-buffered in TMEM) -- nothing else on its critical path;
@@ -35,8 +35,7 @@
 #include "pgx_grid_common.cuh"
 #include "pgx_tc_coeffs.cuh"
 #include "pgx_tc_common.cuh"
-#include "pgx_tc_pass2.cuh"  // kTc2* constants (the tile / record layout shared with pass 1)
-#include "pgx_tc_sweep.cuh"  // f32x2 helpers, mbar_spin
+#include "pgx_tc_shared.cuh"
 
 namespace pgx {
 
@@ -132,7 +131,7 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
     }
     for (int b = 0; b < kTc2S; ++b) {
       mbar_init(&bar_s[b], 1);
-      mbar_init(&bar_p[b], kTc2Epi / 32);
+      mbar_init(&bar_p[b], 4);  // the four warps of the tile's group
     }
     mbar_init(&bar_end, 1);
     fence_mbar_init();
@@ -244,10 +243,13 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
       if (cs.n < nitems) issue_s();  // item k + 3 into the S stage item k just released
     }
   } else {
-    // ======================= epilogue warps
-    const int q = warp & 3, h = warp >> 2;  // lane quarter, pixel half
-    const int i = gbase + 32 * q + lane;     // this thread's grain (TMEM lane)
-    const int g0w = gbase + 32 * q;          // the warp's first grain
+    // ======================= epilogue warps: two groups of four (one warp per
+    // TMEM lane quarter) take alternate tiles, all 64 pixels each, so that a
+    // warp does twice the work per synchronisation and the two groups' waits
+    // interleave instead of coinciding
+    const int q = warp & 3, grp = warp >> 2;  // lane quarter, tile parity
+    const int i = gbase + 32 * q + lane;       // this thread's grain (TMEM lane)
+    const int g0w = gbase + 32 * q;            // the warp's first grain
     const unsigned lane_off = (unsigned)(32 * q) << 16;
     // this grain's fp64 line sums [J] in shared memory (stride 128:
     // conflict-free, no registers held across the tile loop); its gradient rows
@@ -273,102 +275,95 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
 
     const unsigned sbar_s = (unsigned)__cvta_generic_to_shared(&bar_s[0]);
     const unsigned sbar_f = (unsigned)__cvta_generic_to_shared(&bar_full[0]);
-    int sB_next = g.tc_meta[l0 * g.tc_nchunks + blockIdx.x].x;
     float inv = 0.0f;
-    int st = 0, b = 0;
-    unsigned ph_s = 0u, ph_f = 0u;  // phases of the S stage / buffer of the current item
-    Cur c{0, 0, t0}, cf{0, 0, t0};  // current item; item whose group may be flushed (lags by kTc2S)
-    for (; c.n < nitems; c.next(ntiles)) {
-      if (c.t == 0 || c.n == 0) {
-        inv = __int_as_float((127 - (sB_next + 10)) << 23);  // 2^-(sB + 10): S * inv = h~''
-        if (c.li + 1 < nlines) sB_next = g.tc_meta[(l0 + c.li + 1) * g.tc_nchunks + blockIdx.x].x;
+    int li_inv = -1;               // line whose chunk scale `inv` is
+    Cur c{0, 0, t0}, cf{0, 0, t0};  // current item; item whose group may be flushed (group 0)
+    if (grp == 1) c.next(ntiles);
+    for (; c.n < nitems; c.next(ntiles), c.next(ntiles)) {
+      if (c.li != li_inv) {
+        li_inv = c.li;
+        const int sB = __ldg(&g.tc_meta[(l0 + c.li) * g.tc_nchunks + blockIdx.x].x);
+        inv = __int_as_float((127 - (sB + 10)) << 23);  // 2^-(sB + 10): S * inv = h~''
       }
-      const unsigned ts = tmem + 64u * st + lane_off + 32u * h;
-      const float* rec = reinterpret_cast<const float*>(smem + L::REC_OFF + b * L::REC) + 32 * h;
-      mbar_spin(sbar_s + 8u * st, ph_s);
+      const int st = c.n % kTc2S, b = c.n % kGdBuf;
+      const float* rec0 = reinterpret_cast<const float*>(smem + L::REC_OFF + b * L::REC);
+      mbar_spin(sbar_s + 8u * st, (unsigned)(c.n / kTc2S) & 1u);
       tc_fence_after();
-      // UMMA 1 of this item follows UMMA 2 of item n - 3: that group may be final
-      if (c.n >= kTc2S) {
-        if (h == 0 && group_last(cf)) flush(cf);
-        cf.next(ntiles);
-      }
-      uint32_t sv[32];
-      tmem_ld32_nowait(ts, sv);
-      mbar_spin(sbar_f + 8u * b, ph_f);  // records visible
-      // label grains of this warp among the half-tile's pixels (rare)
-      const int lab_x = reinterpret_cast<const int*>(rec)[3 * kTc2Px + lane];
-      const unsigned hit = __ballot_sync(0xffffffffu, (unsigned)(lab_x - g0w) < 32u);
-      tmem_ld_wait();
-      tmem_regs_ready(sv);
+      // UMMA 1 of this item follows UMMA 2 of item n - 3: the groups ending
+      // there are final
+      if (grp == 0)
+        for (; cf.n + kTc2S <= c.n; cf.next(ntiles))
+          if (group_last(cf)) flush(cf);
+      mbar_spin(sbar_f + 8u * b, (unsigned)(c.n / kGdBuf) & 1u);  // records visible
       const unsigned long long ninv2 = f2pack(-inv, -inv);
-      float rr[32];
-#ifdef PGX_GD_NOEPI
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {  // pixel halves [32 h, 32 h + 32)
+        const unsigned ts = tmem + 64u * st + lane_off + 32u * h;
+        const float* rec = rec0 + 32 * h;
+        uint32_t sv[32];
+        tmem_ld32_nowait(ts, sv);
+        // label grains of this warp among the half-tile's pixels (rare)
+        const int lab_x = reinterpret_cast<const int*>(rec)[3 * kTc2Px + lane];
+        const unsigned hit = __ballot_sync(0xffffffffu, (unsigned)(lab_x - g0w) < 32u);
+        tmem_ld_wait();
+        tmem_regs_ready(sv);
+        float rr[32];
 #pragma unroll
-      for (int x = 0; x < 32; ++x) rr[x] = __uint_as_float(sv[x]) * inv;
-#else
-#pragma unroll
-      for (int x4 = 0; x4 < 32; x4 += 4) {
-        const float4 w4 = *reinterpret_cast<const float4*>(rec + x4);
-        const unsigned long long a01 =
-            ffma2(f2pack(__uint_as_float(sv[x4]), __uint_as_float(sv[x4 + 1])), ninv2, f2pack(w4.x, w4.y));
-        const unsigned long long a23 =
-            ffma2(f2pack(__uint_as_float(sv[x4 + 2]), __uint_as_float(sv[x4 + 3])), ninv2, f2pack(w4.z, w4.w));
-        rr[x4] = ex2_approx(f2lo(a01));  // p/2 * 2^13 = 2^(13 + w - h~'')
-        rr[x4 + 1] = ex2_approx(f2hi(a01));
-        rr[x4 + 2] = ex2_approx(f2lo(a23));
-        rr[x4 + 3] = ex2_approx(f2hi(a23));
-      }
-#endif
-      if (hit) {  // label grain: -(1 - p_G)/2 * 2^13 from pass 1 (no cancellation)
-        // the pixels of each distinct in-range label at once (a 32-pixel run
-        // mostly lies in one grain): one round per distinct label, not per pixel
-        const unsigned same = __match_any_sync(0xffffffffu, lab_x);
-        unsigned mine = 0u;
-        for (unsigned m = hit; m;) {
-          const int x = __ffs(m) - 1;
-          const unsigned grp = __shfl_sync(0xffffffffu, same, x);
-          if (__shfl_sync(0xffffffffu, lab_x, x) == i) mine = grp;
-          m &= ~grp;
+        for (int x4 = 0; x4 < 32; x4 += 4) {
+          const float4 w4 = *reinterpret_cast<const float4*>(rec + x4);
+          const unsigned long long a01 =
+              ffma2(f2pack(__uint_as_float(sv[x4]), __uint_as_float(sv[x4 + 1])), ninv2, f2pack(w4.x, w4.y));
+          const unsigned long long a23 =
+              ffma2(f2pack(__uint_as_float(sv[x4 + 2]), __uint_as_float(sv[x4 + 3])), ninv2, f2pack(w4.z, w4.w));
+          rr[x4] = ex2_approx(f2lo(a01));  // p/2 * 2^13 = 2^(13 + w - h~'')
+          rr[x4 + 1] = ex2_approx(f2hi(a01));
+          rr[x4 + 2] = ex2_approx(f2lo(a23));
+          rr[x4 + 3] = ex2_approx(f2hi(a23));
         }
-        if (__any_sync(0xffffffffu, mine != 0u)) {
-          const float* qn = rec + 2 * kTc2Px;
+        if (hit) {  // label grain: -(1 - p_G)/2 * 2^13 from pass 1 (no cancellation)
+          // the pixels of each distinct in-range label at once (a 32-pixel run
+          // mostly lies in one grain): one round per distinct label, not per pixel
+          const unsigned same = __match_any_sync(0xffffffffu, lab_x);
+          unsigned mine = 0u;
+          for (unsigned m = hit; m;) {
+            const int x = __ffs(m) - 1;
+            const unsigned gx = __shfl_sync(0xffffffffu, same, x);
+            if (__shfl_sync(0xffffffffu, lab_x, x) == i) mine = gx;
+            m &= ~gx;
+          }
+          if (__any_sync(0xffffffffu, mine != 0u)) {
+            const float* qn = rec + 2 * kTc2Px;
 #pragma unroll
-          for (int x = 0; x < 32; ++x)
-            if (mine & (1u << x)) rr[x] = qn[x];
+            for (int x = 0; x < 32; ++x)
+              if (mine & (1u << x)) rr[x] = qn[x];
+          }
         }
-      }
-      // exact split: hi = rr with the 13 low mantissa bits cleared (an fp16
-      // value), lo = rr - hi (exact in fp32, |lo| < 2^-10 |rr|) rounded to fp16
-      uint32_t pp[32];  // [0, 16): r'_hi pairs, [16, 32): r'_lo pairs
+        // exact split: hi = rr with the 13 low mantissa bits cleared (an fp16
+        // value), lo = rr - hi (exact in fp32, |lo| < 2^-10 |rr|) rounded to fp16
+        uint32_t pp[32];  // [0, 16): r'_hi pairs, [16, 32): r'_lo pairs
 #pragma unroll
-      for (int cc = 0; cc < 16; ++cc) {
-        const float h0 = __uint_as_float(__float_as_uint(rr[2 * cc]) & 0xffffe000u);
-        const float h1 = __uint_as_float(__float_as_uint(rr[2 * cc + 1]) & 0xffffe000u);
-        const unsigned long long lo2 =
-            ffma2(f2pack(h0, h1), f2pack(-1.0f, -1.0f), f2pack(rr[2 * cc], rr[2 * cc + 1]));
-        pp[cc] = pack_h2(h0, h1);
-        pp[16 + cc] = pack_h2(f2lo(lo2), f2hi(lo2));
+        for (int cc = 0; cc < 16; ++cc) {
+          const float h0 = __uint_as_float(__float_as_uint(rr[2 * cc]) & 0xffffe000u);
+          const float h1 = __uint_as_float(__float_as_uint(rr[2 * cc + 1]) & 0xffffe000u);
+          const unsigned long long lo2 =
+              ffma2(f2pack(h0, h1), f2pack(-1.0f, -1.0f), f2pack(rr[2 * cc], rr[2 * cc + 1]));
+          pp[cc] = pack_h2(h0, h1);
+          pp[16 + cc] = pack_h2(f2lo(lo2), f2hi(lo2));
+        }
+        tmem_st32(ts, pp);
       }
-      tmem_st32(ts, pp);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_p[st]);
-      // next item's stage / buffer and phases
-      if (++st == kTc2S) {
-        st = 0;
-        ph_s ^= 1u;
-      }
-      if (++b == kGdBuf) {
-        b = 0;
-        ph_f ^= 1u;
-      }
     }
     // the last groups: complete once the final commit lands
-    mbar_wait(&bar_end, 0);
-    tc_fence_after();
-    for (; cf.n < nitems; cf.next(ntiles))
-      if (h == 0 && group_last(cf)) flush(cf);
+    if (grp == 0) {
+      mbar_wait(&bar_end, 0);
+      tc_fence_after();
+      for (; cf.n < nitems; cf.next(ntiles))
+        if (group_last(cf)) flush(cf);
+    }
   }
   tc_fence_before();
   __syncthreads();

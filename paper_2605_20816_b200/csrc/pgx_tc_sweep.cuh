@@ -28,15 +28,16 @@
 //   mask) are tracked; s' = sum_{i != G} 2^(ref - h~''_i) with a reference
 //   that moves only when the min falls more than kSwStale below it:
 //   packed FFMA2 (argument pairs) + MUFU.EX2 + packed FADD2 per logit pair.
-// Per pixel at the end: exactly as pass 1 before (pgx_tc_pass1.cuh): the
-// label term in fp64, the exact fp64 tie-tolerant arg-min over the masked
-// columns, the pass-2 record and the per-pixel statistics.
+// Per pixel at the end: the label term in fp64, the exact fp64 tie-tolerant
+// arg-min over the masked columns (a third block as close, or an overflowing
+// candidate list, queues the pixel for the tail's exact re-scan), the pass-2
+// record and the per-pixel statistics.
 #pragma once
 
 #include "pgx_grid_common.cuh"
 #include "pgx_tc_coeffs.cuh"
 #include "pgx_tc_common.cuh"
-#include "pgx_tc_pass1.cuh"  // TcRare, tc_rare_update, kTcThreadsTile
+#include "pgx_tc_shared.cuh"
 
 namespace pgx {
 
@@ -59,41 +60,6 @@ struct SwSmem {
   static constexpr int RING = (BUDGET - IMG_OFF) / IMG < kSwRingMax ? (BUDGET - IMG_OFF) / IMG : kSwRingMax;
   static constexpr int TOTAL = IMG_OFF + RING * IMG;
 };
-
-// packed fp32 pairs (f32x2 SIMD on sm_100: FFMA2 / FADD2)
-__device__ __forceinline__ unsigned long long f2pack(float lo, float hi) {
-  return ((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo);
-}
-__device__ __forceinline__ float f2lo(unsigned long long v) { return __uint_as_float((unsigned)v); }
-__device__ __forceinline__ float f2hi(unsigned long long v) { return __uint_as_float((unsigned)(v >> 32)); }
-__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
-                                                    unsigned long long c) {
-  unsigned long long r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
-  unsigned long long r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-
-// spin on a phase (no suspend hint: the epilogue's waits are short); a lost
-// arrival traps instead of hanging the GPU
-__device__ __forceinline__ void mbar_spin(unsigned addr, unsigned parity) {
-  for (unsigned spin = 0;; ++spin) {
-    unsigned done;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(addr), "r"(parity)
-        : "memory");
-    if (done) return;
-    if (spin == (1u << 28)) __trap();
-  }
-}
 
 template <int DIM, int D>
 __global__ void __launch_bounds__(kSwThreads, 1) k_tc_sweep(GridParams g) {
