@@ -36,3 +36,9 @@ void tc_dispatch_pass2(const GridParams& g, dim3 grid, cudaStream_t s) {
 PGX_INST_GRID(PGX_I)
 
 }  // namespace pgx
+
+#ifdef PGX_GD_TRACE
+extern "C" int pgx_debug_trace(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, pgx::gd_trace, sizeof(pgx::gd_trace));
+}
+#endif
