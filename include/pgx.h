@@ -93,6 +93,13 @@ typedef struct {
     int32_t mem;          /* PGX_MEM_HOST or PGX_MEM_DEVICE for points/labels0  */
     int32_t device;       /* CUDA device ordinal                                */
     void* stream;         /* cudaStream_t (NULL = legacy default stream)        */
+    /* Explicit design matrix (objective.py:129-132 ``design_values``): when not
+     * NULL, design is K x n_points row-major fp64 (K = design_k <= 66, any
+     * features), in host or device memory per ``mem``; dim, basis_kind,
+     * degree, resolution and points are then ignored.  The exact fp64
+     * kernels evaluate it (PGX_PREC_EXACT arithmetic whatever ``precision``). */
+    const double* design;
+    int32_t design_k;
 } pgx_desc;
 
 /* Scalar results of one evaluation (objective.EvalResult, objective.py:90-94,
@@ -150,6 +157,12 @@ pgx_status pgx_eval(pgx_problem* problem, const void* theta, double eps, double 
  * top-2 cost margin; stats_out (nullable) receives n_correct / n_ambiguous. */
 pgx_status pgx_assign(pgx_problem* problem, const void* theta, uint32_t flags,
                       int64_t* labels_out, float* margin_out, pgx_stats* stats_out);
+
+/* Dense soft assignment (objective.py:80-87, a small-problem diagnostic):
+ * prob_out[i * n_points + x] = exp((min_j h_j(x) - h_i(x)) / eps) / sum_j (...),
+ * N x n_points fp64 (host memory unless PGX_DEVICE_PTRS).  eps > 0. */
+pgx_status pgx_soft_assign(pgx_problem* problem, const void* theta, double eps, uint32_t flags,
+                           double* prob_out);
 
 /* Per-grain label moments of a regular 2-D grid (make_grid(resolution)), the
  * input of the moment heuristic (heuristics.py:46-73, np.bincount of 1, x_a and

@@ -26,12 +26,15 @@ from .objective import (
     EvalResult,
     EvalStats,
     Problem,
+    SoftAssignment,
     energy_eps,
     energy_zero,
     evaluate_objective,
     gradient,
     hard_assign,
+    hessian_block,
     objective,
+    soft_assign,
 )
 from .heuristics import MomentSummary, heuristic_theta, moments
 from .optimizer import FitConfig, FitReport, fit, init_zero, line_search
@@ -44,6 +47,6 @@ __all__ = [
     "assemble_design_matrix", "feature_count", "InputFormatError", "NumericalError",
     "ResourceError", "TIE_RTOL", "GrainMap", "PixelGrid", "accuracy_and_error", "make_grid",
     "EvalResult", "EvalStats", "Problem", "energy_eps", "energy_zero", "evaluate_objective",
-    "gradient", "hard_assign", "objective", "FitConfig", "FitReport", "fit", "init_zero",
+    "gradient", "hard_assign", "objective", "soft_assign", "hessian_block", "SoftAssignment", "FitConfig", "FitReport", "fit", "init_zero",
     "line_search", "MomentSummary", "heuristic_theta", "moments",
 ]

@@ -65,6 +65,8 @@ class PgxDesc(ctypes.Structure):
         ("mem", c_int32),
         ("device", c_int32),
         ("stream", c_void_p),
+        ("design", c_void_p),
+        ("design_k", c_int32),
     ]
 
 
@@ -99,6 +101,7 @@ SIGNATURES = {
     "pgx_profile_name": (c_char_p, [c_void_p, c_int]),
     "pgx_profile_ms": (c_float, [c_void_p, c_int]),
     "pgx_synchronize": (c_int, [c_void_p]),
+    "pgx_soft_assign": (c_int, [c_void_p, c_void_p, c_double, c_uint32, c_void_p]),
     "pgx_label_moments": (c_int, [c_int, ctypes.c_int64, c_void_p, c_int, c_void_p]),
     "pgx_label_moments_error": (c_char_p, []),
 }

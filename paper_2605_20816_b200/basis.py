@@ -90,6 +90,26 @@ class DesignBasis:
     def dimension(self) -> int:
         return len(self.index_set)
 
+    def evaluate(self, points) -> np.ndarray:
+        """The (K, n) features of ``points`` on the host (basis.py:105-117), for the
+        small-problem diagnostics only (hessian_block); the hot path regenerates
+        eta(x) on the device and never forms this matrix."""
+        pts = np.asarray(points, dtype=np.float64)
+        d = self.degree
+        tabs = []
+        for j in range(pts.shape[1]):
+            t = pts[:, j]
+            u = np.empty((d + 1,) + t.shape)
+            u[0] = 1.0
+            if d >= 1:
+                u[1] = t
+            for m in range(1, d):  # (m+1) P_{m+1} = (2m+1) t P_m - m P_{m-1}, or powers
+                u[m + 1] = ((2 * m + 1) * t * u[m] - m * u[m - 1]) / (m + 1) if self.kind == LEGENDRE \
+                    else u[m] * t
+            tabs.append(u)
+        return np.asarray([np.prod([tabs[j][a[j]] for j in range(len(a))], axis=0)
+                           for a in self.index_set.indices])
+
 
 @dataclass(frozen=True)
 class DesignMatrix:

@@ -58,6 +58,7 @@ struct pgx_problem {
 
   // device buffers owned by the problem
   double* d_points = nullptr;
+  double* d_design = nullptr;     // explicit K x P design matrix (pgx_desc.design)
   int32_t* d_labels = nullptr;
   double* d_theta = nullptr;      // K x N fp64 working copy
   void* d_theta_in = nullptr;     // host-theta staging (K x N x 8 bytes)
@@ -107,7 +108,7 @@ struct pgx_problem {
     return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(1, n) * sizeof(T));
   }
   void release() {
-    void* bufs[] = {d_points, d_labels, d_theta, d_theta_in, d_pix_m, d_pix_ls, d_fix_list,
+    void* bufs[] = {d_points, d_design, d_labels, d_theta, d_theta_in, d_pix_m, d_pix_ls, d_fix_list,
                     d_counters, d_fix_correct, d_part_th2, d_part_d, d_part_i, d_part_g, d_grad, d_stats,
                     d_labels_out, d_margin_out, grid.d_part, grid.d_tc, grid.d_tc_pix};
     for (void* b : bufs)
@@ -233,6 +234,15 @@ pgx_status stage_theta(pgx_problem* pb, const void* theta, uint32_t flags, const
 
 pgx_status validate_desc(const pgx_desc* d) {
   if (!d) return fail(PGX_ERR_INVALID_ARGUMENT, "descriptor must not be NULL");
+  if (d->design) {  // explicit design matrix: basis and grid fields are ignored
+    if (d->design_k < 1 || d->design_k > kMaxK)
+      return fail(PGX_ERR_INVALID_ARGUMENT, "design_k must lie in [1, %d], got %d", kMaxK, d->design_k);
+    if (d->n_grains < 2) return fail(PGX_ERR_INVALID_ARGUMENT, "a grain map needs at least two grains");
+    if (d->n_grains > (1 << 24)) return fail(PGX_ERR_INVALID_ARGUMENT, "n_grains %d too large", d->n_grains);
+    if (d->n_points < 1 || d->n_points > ((int64_t)1 << 31) - 1)
+      return fail(PGX_ERR_INVALID_ARGUMENT, "n_points out of range");
+    return PGX_OK;
+  }
   if (d->dim != 2 && d->dim != 3)
     return fail(PGX_ERR_INVALID_ARGUMENT, "dim must be 2 or 3, got %d", d->dim);
   if (d->basis_kind != PGX_BASIS_LEGENDRE && d->basis_kind != PGX_BASIS_MONOMIAL)
@@ -263,7 +273,7 @@ pgx_status validate_desc(const pgx_desc* d) {
 
 size_t workspace_estimate(const pgx_desc* d, int sms) {
   const int64_t P = d->n_points;
-  const int K = feature_count(d->dim, d->degree);
+  const int K = d->design ? d->design_k : feature_count(d->dim, d->degree);
   const int64_t KN = (int64_t)K * d->n_grains;
   const int64_t blocks1 = (P + kP1Threads - 1) / kP1Threads;
   const int tiles = (d->n_grains + kP2Threads - 1) / kP2Threads;
@@ -273,7 +283,10 @@ size_t workspace_estimate(const pgx_desc* d, int sms) {
   b += (size_t)P * 4 + (size_t)KN * 8 * 3 + (size_t)P * 8 * 2 + (size_t)P * 4;
   b += (size_t)blocks1 * (16 + 32) + (size_t)splits * KN * 8;
   b += (size_t)P * 12;
-  b += grid_workspace_bytes(d, sms);
+  if (d->design)
+    b += (size_t)P * K * 8;
+  else
+    b += grid_workspace_bytes(d, sms);
   return b;
 }
 
@@ -312,14 +325,15 @@ pgx_status pgx_problem_create(const pgx_desc* desc, pgx_problem** out) {
   PGX_CUDA(cudaSetDevice(desc->device));
 
   pgx_problem* pb = new pgx_problem();
-  pb->dim = desc->dim;
+  const bool design = desc->design != nullptr;
+  pb->dim = design ? 2 : desc->dim;
   pb->kind = desc->basis_kind;
-  pb->degree = desc->degree;
-  pb->K = feature_count(desc->dim, desc->degree);
+  pb->degree = design ? 0 : desc->degree;  // (the tail's kernel instantiation only)
+  pb->K = design ? desc->design_k : feature_count(desc->dim, desc->degree);
   pb->N = desc->n_grains;
   pb->P = desc->n_points;
-  pb->M = desc->resolution;
-  pb->prec = desc->precision;
+  pb->M = design ? -1 : desc->resolution;  // -1: no grid, no point list
+  pb->prec = design ? PGX_PREC_EXACT : desc->precision;
   pb->device = desc->device;
   pb->stream = static_cast<cudaStream_t>(desc->stream);
   const int sms = sm_count(desc->device);
@@ -335,6 +349,7 @@ pgx_status pgx_problem_create(const pgx_desc* desc, pgx_problem** out) {
     if (e == cudaSuccess) e = r;
   };
   if (pb->M == 0) A(pb->alloc(&pb->d_points, (size_t)P * pb->dim));
+  if (design) A(pb->alloc(&pb->d_design, (size_t)P * pb->K));
   A(pb->alloc(&pb->d_labels, (size_t)P));
   A(pb->alloc(&pb->d_theta, (size_t)KN));
   A(pb->alloc(reinterpret_cast<double**>(&pb->d_theta_in), (size_t)KN));
@@ -351,7 +366,7 @@ pgx_status pgx_problem_create(const pgx_desc* desc, pgx_problem** out) {
   A(pb->alloc(&pb->d_stats, 1));
   A(pb->alloc(&pb->d_labels_out, (size_t)P));
   A(pb->alloc(&pb->d_margin_out, (size_t)P));
-  if (e == cudaSuccess) e = grid_plan_create(pb->grid, desc, sms, pb->bytes);
+  if (e == cudaSuccess && !design) e = grid_plan_create(pb->grid, desc, sms, pb->bytes);
   if (e == cudaSuccess) e = cudaMemset(pb->d_counters, 0, 4 * sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(pb->d_fix_correct, 0, 2 * sizeof(long long));
   if (e != cudaSuccess) {
@@ -387,6 +402,14 @@ pgx_status pgx_problem_create(const pgx_desc* desc, pgx_problem** out) {
       pb->release();
       delete pb;
       return fail(PGX_ERR_CUDA, "copying points failed: %s", cudaGetErrorString(c));
+    }
+  }
+  if (design) {
+    cudaError_t c = cudaMemcpy(pb->d_design, desc->design, (size_t)P * pb->K * 8, kind_in);
+    if (c != cudaSuccess) {
+      pb->release();
+      delete pb;
+      return fail(PGX_ERR_CUDA, "copying the design matrix failed: %s", cudaGetErrorString(c));
     }
   }
   // labels: int64 0-based -> int32 on device, range-checked (geometry.py:96-97)
@@ -547,6 +570,19 @@ static pgx_status eval_impl(pgx_problem* pb, const void* theta, double eps, doub
     st = grid_eval(pb->grid, prm, pb->prec, want_grad, s, &launches, &blocks1, prof);
     if (st != PGX_OK) return fail(st, "grid path: %s", cudaGetErrorString(cudaGetLastError()));
     PGX_LAUNCH_CHECK();
+  } else if (pb->d_design) {
+    pb->prof_begin("design_pass1");
+    launch_design_pass1(prm, pb->d_design, pb->K, pb->blocks1, true, s);
+    pb->prof_end();
+    PGX_LAUNCH_CHECK();
+    ++launches;
+    if (want_grad) {
+      pb->prof_begin("design_pass2");
+      launch_design_pass2(prm, pb->d_design, pb->K, pb->splits, s);
+      pb->prof_end();
+      PGX_LAUNCH_CHECK();
+      ++launches;
+    }
   } else {
     pb->prof_begin("general_pass1");
     PGX_DISPATCH(launch_general_pass1, prm, pb->blocks1, true, s);
@@ -637,7 +673,10 @@ pgx_status pgx_assign(pgx_problem* pb, const void* theta, uint32_t flags, int64_
   prm.theta = theta64;
   prm.labels_out = reinterpret_cast<long long*>(dev ? labels_out : (int64_t*)pb->d_labels_out);
   prm.margin_out = margin_out ? (dev ? margin_out : pb->d_margin_out) : nullptr;
-  PGX_DISPATCH(launch_general_pass1, prm, pb->blocks1, false, s);
+  if (pb->d_design)
+    launch_design_pass1(prm, pb->d_design, pb->K, pb->blocks1, false, s);
+  else
+    PGX_DISPATCH(launch_general_pass1, prm, pb->blocks1, false, s);
   PGX_LAUNCH_CHECK();
   ++launches;
   TailParams tp{};
@@ -670,6 +709,38 @@ pgx_status pgx_assign(pgx_problem* pb, const void* theta, uint32_t flags, int64_
       PGX_CUDA(cudaMemcpyAsync(stats_out, pb->d_stats, sizeof(pgx_stats), cudaMemcpyDeviceToHost, s));
     PGX_CUDA(cudaStreamSynchronize(s));
   }
+  return PGX_OK;
+}
+
+pgx_status pgx_soft_assign(pgx_problem* pb, const void* theta, double eps, uint32_t flags, double* prob_out) {
+  g_last_error.clear();
+  if (!pb) return fail(PGX_ERR_INVALID_ARGUMENT, "problem must not be NULL");
+  if (!prob_out) return fail(PGX_ERR_INVALID_ARGUMENT, "prob_out must not be NULL");
+  if (!(eps > 0.0) || !std::isfinite(eps)) return fail(PGX_ERR_INVALID_ARGUMENT, "eps must be positive");
+  const bool dev = flags & PGX_DEVICE_PTRS;
+  PGX_CUDA(cudaSetDevice(pb->device));
+  cudaStream_t s = pb->stream;
+  int launches = 0;
+  const double* theta64 = nullptr;
+  pgx_status st = stage_theta(pb, theta, flags, &theta64, &launches);
+  if (st != PGX_OK) return st;
+  const size_t bytes = (size_t)pb->N * pb->P * 8;
+  double* out = prob_out;
+  if (!dev) PGX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&out), bytes, s));
+  EvalParams prm = make_params(pb, eps);
+  prm.theta = theta64;
+  if (pb->d_design)
+    launch_design_soft(prm, pb->d_design, pb->K, out, s);
+  else
+    PGX_DISPATCH(launch_general_soft, prm, out, s);
+  cudaError_t le = cudaGetLastError();
+  if (!dev) {
+    if (le == cudaSuccess) le = cudaMemcpyAsync(prob_out, out, bytes, cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(out, s);
+    if (le == cudaSuccess) le = cudaStreamSynchronize(s);
+  }
+  if (le != cudaSuccess) return fail(PGX_ERR_CUDA, "soft assignment failed: %s", cudaGetErrorString(le));
+  pb->last_launches = launches + 1;
   return PGX_OK;
 }
 

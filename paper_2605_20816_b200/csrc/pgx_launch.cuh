@@ -77,6 +77,14 @@ void launch_general_pass2(const EvalParams& prm, int N, int splits, cudaStream_t
 template <int DIM, int D>
 void launch_tail(const EvalParams& prm, const TailParams& tp, int blocks, cudaStream_t s);
 
+// explicit design matrix (any K <= kMaxK) and the dense soft assignment: pgx_design.cuh
+void launch_design_pass1(const EvalParams& prm, const double* dsg, int K, int blocks, bool eval,
+                         cudaStream_t s);
+void launch_design_pass2(const EvalParams& prm, const double* dsg, int K, int splits, cudaStream_t s);
+void launch_design_soft(const EvalParams& prm, const double* dsg, int K, double* prob, cudaStream_t s);
+template <int DIM, int D>
+void launch_general_soft(const EvalParams& prm, double* prob, cudaStream_t s);
+
 // regular-grid fp64 path: pgx_grid_pass1.cuh, pgx_grid_pass2.cuh
 template <int DIM, int D>
 void grid_dispatch_pass1(const GridParams& g, int R, int blocks, cudaStream_t s);

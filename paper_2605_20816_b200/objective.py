@@ -88,8 +88,11 @@ class Problem:
 
     def __init__(self, grid, basis_kind: str, degree: int, n_grains: int, labels0=None, *,
                  precision: str | None = None, device: int = 0, stream: int | None = None,
-                 dim: int | None = None):
+                 dim: int | None = None, design=None):
         lib = _lib.load()
+        if design is not None:  # explicit (K, P) design matrix (objective.py:129-132 form)
+            self._init_design(lib, design, n_grains, labels0, device, stream)
+            return
         gdim, res, pts = _grid_spec(grid)
         if dim is not None and dim != gdim:
             raise ValueError(f"grid dimension {gdim} != requested {dim}")
@@ -132,6 +135,41 @@ class Problem:
         self._lock = threading.Lock()
         self._stats = _lib.PgxStats()
         self._spec = (grid, basis_kind, degree, self._labels, int(device), stream, gdim)
+        self._exact = None
+
+    def _init_design(self, lib, design, n_grains, labels0, device, stream):
+        d = np.ascontiguousarray(np.asarray(design, dtype=np.float64))
+        if d.ndim != 2:
+            raise ValueError("design_values must be a (K, P) matrix")
+        self.dim, self.resolution, self.degree, self.basis_kind = 0, 0, -1, None
+        self.K, self.n_points = d.shape
+        self.n_grains = int(n_grains)
+        self.precision = "exact"
+        self._labels = None
+        if labels0 is not None:
+            self._labels = np.ascontiguousarray(np.asarray(labels0, dtype=np.int64))
+            if self._labels.shape != (self.n_points,):
+                raise ValueError(
+                    f"labels length {self._labels.shape[0]} != number of design columns {self.n_points}")
+        self._points = None
+        self._design = d
+        desc = _lib.PgxDesc()
+        desc.n_grains = self.n_grains
+        desc.n_points = self.n_points
+        desc.precision = _lib.PGX_PREC_EXACT
+        desc.labels0 = _lib.as_ptr(self._labels)
+        desc.mem = _lib.PGX_MEM_HOST
+        desc.device = int(device)
+        desc.stream = stream or 0
+        desc.design = d.ctypes.data
+        desc.design_k = self.K
+        handle = ctypes.c_void_p()
+        _lib.check(lib.pgx_problem_create(ctypes.byref(desc), ctypes.byref(handle)))
+        self._lib = lib
+        self._h = handle
+        self._lock = threading.Lock()
+        self._stats = _lib.PgxStats()
+        self._spec = None
         self._exact = None
 
     # ------------------------------------------------------------------ basics
@@ -232,6 +270,17 @@ class Problem:
         _lib.check(self._lib.pgx_eval(self._h, theta_ptr, float(eps), float(lam),
                                       int(flags) | _lib.PGX_DEVICE_PTRS, grad_ptr, stats_ptr))
 
+    def soft_assign(self, theta, eps: float) -> np.ndarray:
+        """Dense (N, P) softmax memberships (objective.py:80-87), pgx_soft_assign."""
+        if not eps > 0:
+            raise ValueError("eps must be positive")
+        t, tflag = self._theta(theta)
+        prob = np.empty((self.n_grains, self.n_points))
+        with self._lock:
+            _lib.check(self._lib.pgx_soft_assign(self._h, t.ctypes.data, float(eps), tflag,
+                                                 prob.ctypes.data))
+        return prob
+
     def assign(self, theta, *, with_margin: bool = False):
         """Tie-tolerant hard assignment (1-based labels) without the N x P costs."""
         t, tflag = self._theta(theta)  # (pgx_assign always runs the exact fp64 kernels)
@@ -274,10 +323,35 @@ def problem_for(design, labels0, n_grains: int, precision: str | None = None) ->
         return prob
 
 
+_DCACHE: list = []
+
+
+def problem_for_design(design_values, labels0, n_grains: int) -> Problem:
+    """Problem handle for an explicit (K, P) design matrix, reused while the
+    same matrix and labels come back (the reference's evaluate_objective
+    callers pass one design for a whole fit)."""
+    d = np.asarray(design_values, dtype=np.float64)
+    lab = None if labels0 is None else np.asarray(labels0, dtype=np.int64)
+    with _CACHE_LOCK:
+        for entry in _DCACHE:
+            dd, n, ll, prob = entry
+            if n == n_grains and dd.shape == d.shape and np.array_equal(dd, d) and (
+                    (ll is None and lab is None) or (ll is not None and lab is not None
+                                                     and np.array_equal(ll, lab))):
+                return prob
+        prob = Problem(None, None, 0, n_grains, lab, design=d)
+        _DCACHE.insert(0, (d.copy(), n_grains, None if lab is None else lab.copy(), prob))
+        while len(_DCACHE) > _CACHE_MAX:
+            _DCACHE.pop()[-1].close()
+        return prob
+
+
 def clear_cache():
     with _CACHE_LOCK:
         while _CACHE:
             _CACHE.pop()[-1].close()
+        while _DCACHE:
+            _DCACHE.pop()[-1].close()
 
 
 # ---------------------------------------------------------------- public API
@@ -304,11 +378,11 @@ def evaluate_objective(theta_values, design, labels0, eps, *, want_grad: bool = 
     and ``chunk_size`` are accepted for signature parity: the device
     reduction is fixed-order and bit-reproducible regardless.
     """
-    if isinstance(design, np.ndarray):
-        raise TypeError("pass the DesignMatrix (not design.values): features are regenerated "
-                        "on the device from design.grid")
     theta_values = np.asarray(theta_values)
-    prob = problem_for(design, labels0, theta_values.shape[1], precision)
+    if isinstance(design, np.ndarray):  # explicit (K, P) design values (objective.py:129-132)
+        prob = problem_for_design(design, labels0, theta_values.shape[1])
+    else:
+        prob = problem_for(design, labels0, theta_values.shape[1], precision)
     res, _ = prob.eval(theta_values, eps, lam=lam, want_grad=want_grad, want_assign=want_assign)
     return res
 
@@ -350,6 +424,60 @@ def hard_assign(theta, basis, grid, design=None) -> np.ndarray:
     d.grid, d.basis = grid, basis
     prob = problem_for(d, None, theta.values.shape[1])
     return prob.assign(theta.values)
+
+
+class SoftAssignment:
+    """objective.SoftAssignment (objective.py:33-51): column x holds (p_i(x))_i."""
+
+    def __init__(self, probabilities, epsilon: float):
+        if epsilon <= 0:
+            raise ValueError("epsilon must be positive")
+        self.probabilities = probabilities
+        self.epsilon = epsilon
+
+    def validate(self, tol: float = 1e-12) -> None:
+        p = self.probabilities
+        if np.any(p <= 0.0) or np.any(p >= 1.0):
+            raise ValueError("soft assignment entries must lie strictly in (0, 1)")
+        if np.abs(p.sum(axis=0) - 1.0).max() > tol:
+            raise ValueError("soft assignment columns must sum to one")
+
+
+def _problem_of(design, n_grains: int) -> Problem:
+    """A label-free problem for a DesignMatrix (lazy or the reference's)."""
+    if getattr(design, "grid", None) is not None and getattr(design, "basis", None) is not None:
+        return problem_for(design, None, n_grains)
+    return problem_for_design(np.asarray(design.values if hasattr(design, "values") else design),
+                              None, n_grains)
+
+
+def soft_assign(theta, design, eps: float) -> SoftAssignment:
+    """Softmax memberships at temperature eps (objective.py:80-87), computed on the
+    device (pgx_soft_assign): dense (N, P), for small problems like the reference's."""
+    if eps <= 0:
+        raise ValueError("eps must be positive")
+    _check_compatible(theta, design)
+    _check_theta(theta)
+    return SoftAssignment(_problem_of(design, theta.values.shape[1]).soft_assign(theta.values, eps),
+                          epsilon=eps)
+
+
+def hessian_block(theta, design, grain_map, eps: float, i: int, k: int) -> np.ndarray:
+    """The (i, k) block of the Hessian (objective.py:201-217), grain indices
+    1-based: -(1/(eps^2 n)) sum_x p_i(x) (1[i==k] - p_k(x)) eta(x) eta(x)^T.
+    A small-problem diagnostic: p from the device soft assignment, the K x K
+    contraction of the (host) features on the host."""
+    n_grains = theta.values.shape[1]
+    if not (1 <= i <= n_grains and 1 <= k <= n_grains):
+        raise ValueError(f"grain indices must lie in 1..{n_grains}")
+    p = soft_assign(theta, design, eps).probabilities
+    pi, pk = p[i - 1], p[k - 1]
+    w = pi * ((1.0 if i == k else 0.0) - pk)
+    try:
+        d = np.asarray(design.values)
+    except AttributeError:
+        d = design.basis.evaluate(np.asarray(design.grid.points))
+    return -(d * w[None, :]) @ d.T / (eps * eps * d.shape[1])
 
 
 def energy_eps(theta, design, grain_map, eps: float) -> float:

@@ -454,3 +454,35 @@ def test_pinned_results_zero_copy_bitwise(pgb, prec):
         np.testing.assert_array_equal(g_pin.numpy(), g_page)
         np.testing.assert_array_equal(s_pin.numpy(), s_page)
     pr.close()
+
+
+def test_design_values_form_vs_oracle(pgb):
+    """evaluate_objective(theta_values, design_values, labels0, eps) with an
+    explicit (K, P) design (objective.py:129-132; the reference's own tests call
+    it this way): any features, K not a basis size."""
+    rng = np.random.default_rng(5)
+    for k, n, p in ((3, 4, 300), (7, 13, 1000), (40, 9, 257), (66, 3, 50)):
+        d = rng.normal(size=(k, p))
+        th = rng.normal(size=(k, n)) * 0.5
+        lab = rng.integers(0, n, p)
+        ref = oracle.evaluate_objective(th, d, lab, 0.3, want_grad=True, want_assign=True)
+        res = pgb.evaluate_objective(th, d, lab, 0.3, want_grad=True, want_assign=True)
+        assert abs(res.phi - ref.phi) <= 1e-12 * (1 + abs(ref.phi))
+        assert np.abs(res.grad - ref.grad).max() <= 1e-10 * np.abs(ref.grad).max()
+        assert res.err == ref.err and res.e0 == pytest.approx(ref.e0, rel=1e-12, abs=1e-14)
+
+
+def test_soft_assign_vs_oracle(pgb):
+    """soft_assign (objective.py:80-87) on the device: dense (N, P) memberships."""
+    rng = np.random.default_rng(6)
+    grid = pgb.make_grid(5)
+    basis = pgb.DesignBasis.make("legendre", 2)
+    design = pgb.assemble_design_matrix(basis, grid)
+    th = pgb.ParamMatrix(rng.normal(size=(6, 7)), basis)
+    soft = pgb.soft_assign(th, design, 0.2)
+    soft.validate()
+    c = th.values.T @ oracle.design_values("legendre", 2, oracle.grid_points(5))
+    z = np.exp((c.min(axis=0)[None] - c) / 0.2)
+    assert np.abs(soft.probabilities - z / z.sum(axis=0)).max() <= 1e-14
+    zero = pgb.soft_assign(pgb.ParamMatrix(np.zeros((6, 5)), basis), design, 0.3)
+    assert np.all(zero.probabilities == 0.2)
