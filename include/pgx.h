@@ -174,6 +174,16 @@ pgx_status pgx_label_moments(int resolution, int64_t n_points, const int64_t* la
                              int64_t* out);
 const char* pgx_label_moments_error(void);
 
+/* The same sums from a problem handle: a regular 2-D grid problem created with
+ * labels (its device-resident labels are used: no label upload, no allocation,
+ * stream-ordered on the problem's stream).  out: n_grains x 6 int64, host
+ * memory (the call then synchronises) or device memory with PGX_DEVICE_PTRS. */
+pgx_status pgx_problem_label_moments(pgx_problem* problem, uint32_t flags, int64_t* out);
+
+/* Bytes of device memory the problem actually holds (equals
+ * pgx_workspace_bytes of its descriptor up to small per-buffer rounding). */
+size_t pgx_problem_bytes(pgx_problem* problem);
+
 /* Which kernel family pgx_eval runs for this problem (fixed at creation):
  * PGX_PATH_GENERAL (fp64 CUDA-core kernels over any point list; the exact
  * mode, and the fallback of the fast modes where the grid paths do not

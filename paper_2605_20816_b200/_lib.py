@@ -104,6 +104,8 @@ SIGNATURES = {
     "pgx_soft_assign": (c_int, [c_void_p, c_void_p, c_double, c_uint32, c_void_p]),
     "pgx_label_moments": (c_int, [c_int, ctypes.c_int64, c_void_p, c_int, c_void_p]),
     "pgx_label_moments_error": (c_char_p, []),
+    "pgx_problem_label_moments": (c_int, [c_void_p, c_uint32, c_void_p]),
+    "pgx_problem_bytes": (c_size_t, [c_void_p]),
 }
 
 _lib = None

@@ -17,7 +17,8 @@
 
 namespace pgx {
 
-__global__ void k_label_moments(int M, int64_t P, const int64_t* __restrict__ labels0, int N,
+template <typename LabelT>
+__global__ void k_label_moments(int M, int64_t P, const LabelT* __restrict__ labels0, int N,
                                 unsigned long long* __restrict__ out, int* __restrict__ bad) {
   const int side = 2 * M;
   const unsigned lane = threadIdx.x & 31u;
@@ -56,6 +57,19 @@ __global__ void k_label_moments(int M, int64_t P, const int64_t* __restrict__ la
   }
 }
 
+// Stream-ordered launch over labels already resident on the device (the
+// problem handle's int32 copy): zeroes out / bad, then accumulates.
+cudaError_t launch_label_moments_i32(int M, int64_t P, const int32_t* labels0, int N,
+                                     unsigned long long* out, int* bad, int sms, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(out, 0, (size_t)N * 6 * sizeof(unsigned long long), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0, sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  const int64_t want = (P + 255) / 256;
+  const int blocks = (int)(want < 8LL * sms ? want : 8LL * sms);
+  k_label_moments<int32_t><<<blocks, 256, 0, s>>>(M, P, labels0, N, out, bad);
+  return cudaGetLastError();
+}
+
 }  // namespace pgx
 
 namespace {
@@ -89,11 +103,12 @@ extern "C" pgx_status pgx_label_moments(int resolution, int64_t n_points, const 
     return fail(e);
   cudaMemset(d_out, 0, (size_t)n_grains * 6 * sizeof(unsigned long long));
   cudaMemset(d_bad, 0, sizeof(int));
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t want = (n_points + 255) / 256;
   const int blocks = (int)(want < 8LL * sms ? want : 8LL * sms);
-  pgx::k_label_moments<<<blocks, 256>>>(resolution, n_points, d_lab, n_grains, d_out, d_bad);
+  pgx::k_label_moments<int64_t><<<blocks, 256>>>(resolution, n_points, d_lab, n_grains, d_out, d_bad);
   if ((e = cudaGetLastError()) != cudaSuccess) return fail(e);
   int bad = 0;
   if ((e = cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost)) != cudaSuccess) return fail(e);

@@ -75,6 +75,7 @@ struct pgx_problem {
   pgx_stats* d_stats = nullptr;   // host-mode staging
   long long* d_labels_out = nullptr;
   float* d_margin_out = nullptr;
+  unsigned long long* d_moments = nullptr;  // N x 6 label-moment sums + 1 flag word (2-D grids)
   // true between the first launch of a call and its tail launch: a call that
   // failed in between leaves the fix-up / ticket counters armed, and the next
   // call re-zeroes them first (normally the tail's last CTA re-arms them)
@@ -110,7 +111,7 @@ struct pgx_problem {
   void release() {
     void* bufs[] = {d_points, d_design, d_labels, d_theta, d_theta_in, d_pix_m, d_pix_ls, d_fix_list,
                     d_counters, d_fix_correct, d_part_th2, d_part_d, d_part_i, d_part_g, d_grad, d_stats,
-                    d_labels_out, d_margin_out, grid.d_part, grid.d_tc, grid.d_tc_pix};
+                    d_labels_out, d_margin_out, d_moments, grid.d_part, grid.d_tc, grid.d_tc_pix};
     for (void* b : bufs)
       if (b) cudaFree(b);
     grid_plan_destroy(grid);
@@ -366,6 +367,7 @@ pgx_status pgx_problem_create(const pgx_desc* desc, pgx_problem** out) {
   A(pb->alloc(&pb->d_stats, 1));
   A(pb->alloc(&pb->d_labels_out, (size_t)P));
   A(pb->alloc(&pb->d_margin_out, (size_t)P));
+  if (pb->M > 0 && pb->dim == 2) A(pb->alloc(&pb->d_moments, (size_t)pb->N * 6 + 1));
   if (e == cudaSuccess && !design) e = grid_plan_create(pb->grid, desc, sms, pb->bytes);
   if (e == cudaSuccess) e = cudaMemset(pb->d_counters, 0, 4 * sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(pb->d_fix_correct, 0, 2 * sizeof(long long));
@@ -457,6 +459,26 @@ pgx_status pgx_set_stream(pgx_problem* pb, void* stream) {
   if (!pb) return fail(PGX_ERR_INVALID_ARGUMENT, "problem must not be NULL");
   pb->stream = static_cast<cudaStream_t>(stream);
   return PGX_OK;
+}
+
+size_t pgx_problem_bytes(pgx_problem* pb) { return pb ? pb->bytes : 0; }
+
+pgx_status pgx_problem_label_moments(pgx_problem* pb, uint32_t flags, int64_t* out) {
+  g_last_error.clear();
+  if (!pb || !out) return fail(PGX_ERR_INVALID_ARGUMENT, "problem and out must not be NULL");
+  if (!pb->d_moments || !pb->has_labels)
+    return fail(PGX_ERR_INVALID_ARGUMENT,
+                "label moments need a regular 2-D grid problem created with labels");
+  PGX_CUDA(cudaSetDevice(pb->device));
+  int* bad = reinterpret_cast<int*>(pb->d_moments + (size_t)pb->N * 6);
+  PGX_CUDA(launch_label_moments_i32(pb->M, pb->P, pb->d_labels, pb->N, pb->d_moments, bad, pb->sms, pb->stream));
+  pb->last_launches = 1;
+  const size_t nb = (size_t)pb->N * 6 * sizeof(int64_t);
+  const bool dev = (flags & PGX_DEVICE_PTRS) != 0;
+  PGX_CUDA(cudaMemcpyAsync(out, pb->d_moments, nb, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                           pb->stream));
+  if (!dev) PGX_CUDA(cudaStreamSynchronize(pb->stream));
+  return PGX_OK;  // (labels were range-checked at creation: the flag word cannot be set)
 }
 
 int pgx_last_launch_count(pgx_problem* pb) { return pb ? pb->last_launches : 0; }

@@ -158,48 +158,68 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
   }
 }
 
+// byte sizes of the plan's allocations (one place: the estimate reported with
+// PGX_ERR_RESOURCE is exactly what grid_plan_create asks for)
+struct GridBytes {
+  size_t part = 0;    // gradient partial slots (doubles)
+  size_t main = 0;    // part_g | per-pixel scratch (16 B per pixel)
+  size_t ncoef = 0, nimg = 0, nmeta = 0, nlc = 0;
+  size_t tc = 0;      // coef | img | meta | line factors (PGX_PREC_TC)
+  size_t pix = 0;     // pass-2 pixel operand tiles (PGX_PREC_TC)
+  size_t total() const { return main + tc + pix; }
+};
+
+inline GridBytes grid_bytes(const GridPlan& gp, const pgx_desc* d) {
+  GridBytes b;
+  if (!gp.enabled) return b;
+  const int K = feature_count(d->dim, d->degree);
+  b.part = (size_t)std::max(gp.splits, gp.part_splits) * K * d->n_grains;
+  b.main = b.part * 8 + (size_t)d->n_points * 16 + 256;
+  if (gp.tc) {
+    const int J = d->degree + 1;
+    const size_t nchunks = (d->n_grains + kTcCoefChunk - 1) / kTcCoefChunk;
+    b.ncoef = (size_t)gp.lines * d->n_grains * J;
+    b.nimg = (size_t)gp.lines * nchunks * tc_ksteps(J) * kTcCoefChunk * 32;
+    b.nmeta = (size_t)gp.lines * nchunks;
+    b.nlc = (size_t)gp.lines * K;
+    b.tc = b.ncoef * 8 + b.nimg + b.nmeta * 8 + b.nlc * 8 + 256;
+    if (gp.tc2_splits > 0)
+      b.pix = (size_t)(2 * d->resolution / kTcPixTile) *
+              (tc_ksteps(J) * kTcPixTile * 32 + 2 * (kTcPixTile / 16) * 16 * 32);
+  }
+  return b;
+}
+
 inline size_t grid_workspace_bytes(const pgx_desc* d, int sms) {
   GridPlan gp;
   grid_plan_shape(gp, d, sms);
-  if (!gp.enabled) return 0;
-  const int K = feature_count(d->dim, d->degree);
-  return (size_t)std::max(gp.splits, gp.part_splits) * K * d->n_grains * 8 + (size_t)d->n_points * 16;
+  return grid_bytes(gp, d).total();
 }
 
 inline cudaError_t grid_plan_create(GridPlan& gp, const pgx_desc* d, int sms, size_t& bytes) {
   grid_plan_shape(gp, d, sms);
   if (!gp.enabled) return cudaSuccess;
-  const int K = feature_count(d->dim, d->degree);
-  const size_t part = (size_t)std::max(gp.splits, gp.part_splits) * K * d->n_grains;
-  const size_t n = part * 8 + (size_t)d->n_points * 16 + 256;
-  cudaError_t e = cudaMalloc(&gp.d_part, n);
+  const GridBytes b = grid_bytes(gp, d);
+  cudaError_t e = cudaMalloc(&gp.d_part, b.main);
   if (e != cudaSuccess) return e;
-  bytes += n;
+  bytes += b.main;
   gp.part_out = static_cast<double*>(gp.d_part);
-  gp.pix_w = gp.part_out + part;
+  gp.pix_w = gp.part_out + b.part;
   gp.pix_q = reinterpret_cast<float*>(gp.pix_w + d->n_points);
   if (gp.tc) {
-    const int J = d->degree + 1;
     gp.tc_nchunks = (d->n_grains + kTcCoefChunk - 1) / kTcCoefChunk;
-    const size_t ncoef = (size_t)gp.lines * d->n_grains * J;
-    const size_t nimg = (size_t)gp.lines * gp.tc_nchunks * tc_ksteps(J) * kTcCoefChunk * 32;
-    const size_t nmeta = (size_t)gp.lines * gp.tc_nchunks;
-    const size_t nlc = (size_t)gp.lines * K;
-    const size_t tb = ncoef * 8 + nimg + nmeta * 8 + nlc * 8 + 256;
-    e = cudaMalloc(&gp.d_tc, tb);
+    e = cudaMalloc(&gp.d_tc, b.tc);
     if (e != cudaSuccess) return e;
-    bytes += tb;
+    bytes += b.tc;
     gp.tc_coef = static_cast<double*>(gp.d_tc);
-    gp.tc_img = reinterpret_cast<unsigned char*>(gp.tc_coef + ncoef);
-    gp.tc_meta = reinterpret_cast<int2*>(gp.tc_img + nimg);
-    gp.tc_lc = reinterpret_cast<double*>(gp.tc_meta + nmeta);
+    gp.tc_img = reinterpret_cast<unsigned char*>(gp.tc_coef + b.ncoef);
+    gp.tc_meta = reinterpret_cast<int2*>(gp.tc_img + b.nimg);
+    gp.tc_lc = reinterpret_cast<double*>(gp.tc_meta + b.nmeta);
     if (gp.tc2_splits > 0) {
       gp.tc_rec = reinterpret_cast<float*>(gp.pix_w);  // 16 bytes per pixel
-      const size_t npix = (size_t)(2 * d->resolution / kTcPixTile) *
-                          (tc_ksteps(J) * kTcPixTile * 32 + 2 * (kTcPixTile / 16) * 16 * 32);
-      e = cudaMalloc(&gp.d_tc_pix, npix);
+      e = cudaMalloc(&gp.d_tc_pix, b.pix);
       if (e != cudaSuccess) return e;
-      bytes += npix;
+      bytes += b.pix;
       gp.tc_pix = static_cast<unsigned char*>(gp.d_tc_pix);
       gp.tc_pix_ready = false;
     }

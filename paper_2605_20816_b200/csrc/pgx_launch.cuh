@@ -85,6 +85,10 @@ void launch_design_soft(const EvalParams& prm, const double* dsg, int K, double*
 template <int DIM, int D>
 void launch_general_soft(const EvalParams& prm, double* prob, cudaStream_t s);
 
+// label moments over a problem's resident int32 labels: k_moments.cu
+cudaError_t launch_label_moments_i32(int M, int64_t P, const int32_t* labels0, int N,
+                                     unsigned long long* out, int* bad, int sms, cudaStream_t s);
+
 // regular-grid fp64 path: pgx_grid_pass1.cuh, pgx_grid_pass2.cuh
 template <int DIM, int D>
 void grid_dispatch_pass1(const GridParams& g, int R, int blocks, cudaStream_t s);

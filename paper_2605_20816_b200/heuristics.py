@@ -54,14 +54,18 @@ def _sym2x2_eigvals(b: np.ndarray) -> np.ndarray:
     return np.stack([half_tr - disc, half_tr + disc], axis=-1)
 
 
-def label_moment_sums(grid, labels0: np.ndarray, n_grains: int) -> np.ndarray | None:
+def label_moment_sums(grid, labels0: np.ndarray, n_grains: int, problem=None) -> np.ndarray | None:
     """(N, 6) int64 sums of {1, a1, a2, a1^2, a1 a2, a2^2} per grain with
-    a = 2M x, on the device (regular 2-D grids); None for other point sets."""
+    a = 2M x, on the device (regular 2-D grids); None for other point sets.
+    With ``problem`` (a Problem holding these labels) the sums come from its
+    device-resident labels: no upload, no allocation."""
     from .objective import _grid_spec
 
     dim, res, _ = _grid_spec(grid)  # res > 0 only for make_grid's regular grid
     if dim != 2 or not res:
         return None
+    if problem is not None:
+        return problem.label_moments()
     labels0 = np.ascontiguousarray(labels0, dtype=np.int64)
     if labels0.shape[0] != 4 * int(res) ** 2:
         return None
@@ -75,12 +79,12 @@ def label_moment_sums(grid, labels0: np.ndarray, n_grains: int) -> np.ndarray | 
     return out
 
 
-def moments(grain_map) -> MomentSummary:
+def moments(grain_map, problem=None) -> MomentSummary:
     """Pixel counts, centroids and central second-moment matrices per grain
     (heuristics.py:46-73)."""
     n = int(grain_map.n_grains)
     lab0 = np.asarray(grain_map.labels, dtype=np.int64) - 1
-    sums = label_moment_sums(grain_map.grid, lab0, n)
+    sums = label_moment_sums(grain_map.grid, lab0, n, problem)
     if sums is not None:
         m2 = int(round(math.sqrt(lab0.shape[0])))  # 2M
         counts = sums[:, 0].copy()
@@ -205,14 +209,14 @@ def _monomial_theta(summary: MomentSummary, degree: int, n_pixels: int) -> np.nd
     return theta
 
 
-def heuristic_theta(grain_map, degree: int, kind: str = LEGENDRE) -> ParamMatrix:
+def heuristic_theta(grain_map, degree: int, kind: str = LEGENDRE, *, problem=None) -> ParamMatrix:
     """Moment-based initial coefficients for a degree-d fit, gauge-fixed
     (heuristics.py:95-125)."""
     if degree < 1:
         raise ValueError("heuristic initialisation needs degree >= 1")
     if kind not in (LEGENDRE, MONOMIAL):
         raise ValueError(f"unknown basis kind {kind!r}")
-    summary = moments(grain_map)
+    summary = moments(grain_map, problem)
     mono = _monomial_theta(summary, degree, len(grain_map.labels))
     padded = np.zeros((math.comb(degree + 2, 2), summary.n_grains))  # zero_pad (basis.py:330-344)
     padded[: mono.shape[0]] = mono

@@ -222,6 +222,19 @@ class Problem:
             self.set_profiling(False)
         return res, st, names
 
+    def device_bytes(self) -> int:
+        """Bytes of device memory the handle holds (pgx_problem_bytes)."""
+        return int(self._lib.pgx_problem_bytes(self._h))
+
+    def label_moments(self) -> np.ndarray:
+        """(N, 6) exact int64 sums of {1, a1, a2, a1^2, a1 a2, a2^2} per grain over
+        the problem's resident labels (pgx_problem_label_moments; regular 2-D
+        grids; heuristics.py:46-73 is the bincount form)."""
+        out = np.zeros((self.n_grains, 6), dtype=np.int64)
+        with self._lock:
+            _lib.check(self._lib.pgx_problem_label_moments(self._h, 0, out.ctypes.data))
+        return out
+
     def last_launch_count(self) -> int:
         return int(self._lib.pgx_last_launch_count(self._h))
 
