@@ -37,3 +37,9 @@ PGX_INST_GRID(PGX_I)
 
 }  // namespace pgx
 
+
+#ifdef PGX_GD_TRACE
+extern "C" int pgx_debug_trace(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, pgx::gd_trace, sizeof(pgx::gd_trace));
+}
+#endif

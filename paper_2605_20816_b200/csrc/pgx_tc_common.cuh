@@ -127,6 +127,19 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// one thread of the (converged) warp: the predicate of elect.sync tells the
+// compiler that the guarded region runs single-threaded, so tcgen05.mma /
+// commit are issued without a per-instruction election loop
+__device__ __forceinline__ bool elect_one() {
+  unsigned pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ----------------------------------------------------------------- UMMA
 // shared-memory matrix descriptor (K-major, SWIZZLE_NONE, version 1 = sm_100)
 __device__ __forceinline__ uint64_t umma_desc(unsigned smem_addr) {

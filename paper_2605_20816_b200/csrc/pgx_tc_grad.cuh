@@ -45,6 +45,21 @@ constexpr int kGdBuf = 8;
 constexpr int kGdA = 3;    // coefficient-image slots (lines in flight)
 constexpr int kGdMmaWarp = kTc2Epi / 32, kGdLoadWarp = kGdMmaWarp + 1;
 constexpr int kGdThreads = kTc2Epi + 64;  // + MMA warp + loader warp
+// epilogue work split: true = every item is shared by all 8 warps (warp =
+// lane quarter x pixel half), so two finished S stages always wait ahead of
+// the epilogue; false = two groups of 4 warps on alternate items
+#ifndef PGX_GD_HALVES
+#define PGX_GD_HALVES 1
+#endif
+constexpr bool kGdHalves = PGX_GD_HALVES != 0;
+#ifdef PGX_GD_TRACE
+// experiment builds only (tools/gd_trace.py): clock64 stamps of one CTA's first 256 items
+__device__ long long gd_trace[14][256];
+#define GD_STAMP(e, n) \
+  do { if (blockIdx.x == 3 && blockIdx.y == 5 && (n) < 256) gd_trace[e][n] = clock64(); } while (0)
+#else
+#define GD_STAMP(e, n) do { } while (0)
+#endif
 
 template <int DIM, int D>
 struct GdSmem {
@@ -60,6 +75,24 @@ struct GdSmem {
   static constexpr int R_OFF = REC_OFF + kGdBuf * REC;  // fp64 [J][128] line sums
   static constexpr int TOTAL = R_OFF + J * kTc2Grains * 8;
 };
+
+// program-ordered variants: a warp issues in order, and MUFU.EX2 (8 cycles per
+// warp instruction on its pipe) and F2FP (~5) block the instructions behind
+// them, so the epilogue interleaves the exponentials of one pixel pair with
+// the conversions of an earlier pair; volatile keeps that order
+__device__ __forceinline__ float ex2_ordered(float x) {
+  float y;
+  asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_h2_ordered(float a, float b) {
+  uint32_t r;
+  asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
+#ifndef PGX_GD_ILV
+#define PGX_GD_ILV 1
+#endif
 
 // fp16 pair of two fp32 values, low half = a (the even pixel)
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
@@ -131,7 +164,7 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
     }
     for (int b = 0; b < kTc2S; ++b) {
       mbar_init(&bar_s[b], 1);
-      mbar_init(&bar_p[b], 4);  // the four warps of the tile's group
+      mbar_init(&bar_p[b], kGdHalves ? 8 : 4);  // the warps that write the tile's r'
     }
     mbar_init(&bar_end, 1);
     fence_mbar_init();
@@ -194,54 +227,79 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
       __syncwarp();
     }
   } else if (warp == kGdMmaWarp) {
-    // ======================= MMA warp (warp-uniform loop, one lane issues)
-    const bool leader = lane == 0;
-    const uint64_t d_a1 = umma_desc(sbase + L::A1_OFF);
-    const uint64_t d_pix = umma_desc(sbase + L::PIX_OFF);
-    Cur cs{0, 0, t0}, cm{0, 0, t0};  // next UMMA 1, next UMMA 2
-    auto issue_s = [&]() {  // UMMA 1 of item cs into S_(n % 3)
-      const int b = cs.n % kGdBuf, st = cs.n % kTc2S, ab = cs.li % kGdA;
-      if (cs.t == 0 || cs.n == 0) mbar_wait(&bar_a[ab], (unsigned)(cs.li / kGdA) & 1u);
-      mbar_wait(&bar_full[b], (unsigned)(cs.n / kGdBuf) & 1u);
-      tc_fence_after();
-      if (leader) {
+    // ======================= MMA issuer: ONE thread runs the whole role (no
+    // warp-level re-convergence inside the loop), and every tcgen05 operand is
+    // derived from warp-uniform values (the TMEM base broadcast by a shuffle),
+    // so that each MMA is a single UTCHMMA on uniform registers instead of an
+    // elect / broadcast loop: the issuer's per-item time bounds the kernel
+    const unsigned tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+    const unsigned sbase_u = __shfl_sync(0xffffffffu, sbase, 0);
+    if (elect_one()) {
+      const uint64_t d_a1 = umma_desc(sbase_u + L::A1_OFF);
+      const uint64_t d_pix = umma_desc(sbase_u + L::PIX_OFF);
+      Cur cs{0, 0, t0}, cm{0, 0, t0};  // next UMMA 1, next UMMA 2
+      int cs_st = 0, cs_b = 0;         // cs.n % kTc2S, cs.n % kGdBuf
+      auto issue_s = [&]() {  // UMMA 1 of item cs into S_(n % 3)
+        const int ab = cs.li % kGdA;
+        if (cs.t == 0 || cs.n == 0) mbar_wait(&bar_a[ab], (unsigned)(cs.li / kGdA) & 1u);
+        mbar_wait(&bar_full[cs_b], (unsigned)(cs.n / kGdBuf) & 1u);
+        tc_fence_after();
         const uint64_t da = d_a1 + (uint64_t)((ab * L::A1) >> 4);
-        const uint64_t db = d_pix + (uint64_t)((b * L::PIX) >> 4);
+        const uint64_t db = d_pix + (uint64_t)((cs_b * L::PIX) >> 4);
 #pragma unroll
         for (int s = 0; s < KS; ++s)
-          umma_f16_ss(tmem + 64u * st, da + (uint64_t)((s * kTc2Grains * 32) >> 4),
+          umma_f16_ss(tmem_u + 64u * cs_st, da + (uint64_t)((s * kTc2Grains * 32) >> 4),
                       db + (uint64_t)((s * kTc2Px * 32) >> 4), IDESC1, s > 0);
-        umma_commit(&bar_s[st]);
+        umma_commit(&bar_s[cs_st]);
         if (cs.t == ntiles - 1 || cs.n == nitems - 1) umma_commit(&bar_af[ab]);  // the line's image is free
-      }
-      __syncwarp();
-      cs.next(ntiles);
-    };
-    while (cs.n < nitems && cs.n < kTc2S) issue_s();
-    for (int k = 0; k < nitems; ++k) {
-      const int st = k % kTc2S, b = k % kGdBuf;
-      mbar_wait(&bar_p[st], (unsigned)(k / kTc2S) & 1u);  // r' of item k is in S_st
-      tc_fence_after();
-      if (leader) {  // UMMA 2: R += [r_hi; r_lo] . [L_hi | L_lo]^T over the 64 pixels
-        const unsigned tr = r_col(cm);
-        const unsigned ts = tmem + 64u * st;
-        const uint64_t dl = d_pix + (uint64_t)((b * L::PIX + KS * (kTc2Px * 32)) >> 4);
-        const bool fresh = (cm.t & (kTc2Group - 1)) == 0 || cm.n == 0;  // a group's first item
+        GD_STAMP(4, cs.n);
+        cs.next(ntiles);
+        if (++cs_st == kTc2S) cs_st = 0;
+        if (++cs_b == kGdBuf) cs_b = 0;
+      };
+      while (cs.n < nitems && cs.n < kTc2S) issue_s();
+      int st = 0, b = 0;
+      unsigned ph_p = 0;  // phase parity of bar_p[st]: flips each time st wraps
+      unsigned rsel = (unsigned)(t0 / kTc2Group) & 1u;  // R accumulator of cm's group (= r_col)
+      for (int k = 0; k < nitems; ++k) {
+        mbar_wait(&bar_p[st], ph_p);  // r' of item k is in S_st
+        tc_fence_after();
+        GD_STAMP(2, k);
+        {  // UMMA 2: R += [r_hi; r_lo] . [L_hi | L_lo]^T over the 64 pixels
+          const unsigned ts = tmem_u + 64u * st;
+          const uint64_t dl = d_pix + (uint64_t)((b * L::PIX + KS * (kTc2Px * 32)) >> 4);
+          const bool fresh = (cm.t & (kTc2Group - 1)) == 0 || cm.n == 0;  // a group's first item
+          auto umma2 = [&](unsigned tr) {
 #pragma unroll
-        for (int s = 0; s < 2 * (kTc2Px / 16); ++s) {
-          const int p = s / (kTc2Px / 16), ks = s % (kTc2Px / 16);
-          // pixels [16 ks, 16 ks + 16): half ks / 2, packed columns 8 (ks % 2); p = 1: r_lo
-          const unsigned a = ts + 32u * (ks >> 1) + 8u * (ks & 1) + (p == 1 ? 16u : 0u);
-          const uint64_t bo = dl + (uint64_t)((ks * 1024) >> 4);
-          umma_f16_ts(tr, a, bo, IDESC2, !(fresh && s == 0));
+            for (int s = 0; s < 2 * (kTc2Px / 16); ++s) {
+              const int p = s / (kTc2Px / 16), ks = s % (kTc2Px / 16);
+              // pixels [16 ks, 16 ks + 16): half ks / 2, packed columns 8 (ks % 2); p = 1: r_lo
+              const unsigned a = ts + 32u * (ks >> 1) + 8u * (ks & 1) + (p == 1 ? 16u : 0u);
+              const uint64_t bo = dl + (uint64_t)((ks * 1024) >> 4);
+              umma_f16_ts(tr, a, bo, IDESC2, !(fresh && s == 0));
+            }
+          };
+          // (one copy per accumulator: a data-dependent D address costs an
+          // elect / broadcast loop per MMA)
+          if (rsel)
+            umma2(tmem_u + 224u);
+          else
+            umma2(tmem_u + 192u);
+          umma_commit(&bar_pf[b]);  // item k's pixel / record buffer is free once UMMA 2 is done
+          if (k == nitems - 1) umma_commit(&bar_end);
+          GD_STAMP(3, k);
         }
-        umma_commit(&bar_pf[b]);  // item k's pixel / record buffer is free once UMMA 2 is done
-        if (k == nitems - 1) umma_commit(&bar_end);
+        cm.next(ntiles);
+        if ((cm.t & (kTc2Group - 1)) == 0) rsel ^= 1u;  // the group index grows by one per boundary
+        if (cs.n < nitems) issue_s();  // item k + 3 into the S stage item k just released
+        if (++st == kTc2S) {
+          st = 0;
+          ph_p ^= 1u;
+        }
+        if (++b == kGdBuf) b = 0;
       }
-      __syncwarp();
-      cm.next(ntiles);
-      if (cs.n < nitems) issue_s();  // item k + 3 into the S stage item k just released
     }
+    __syncwarp();
   } else {
     // ======================= epilogue warps: two groups of four (one warp per
     // TMEM lane quarter) take alternate tiles, all 64 pixels each, so that a
@@ -278,8 +336,8 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
     float inv = 0.0f;
     int li_inv = -1;               // line whose chunk scale `inv` is
     Cur c{0, 0, t0}, cf{0, 0, t0};  // current item; item whose group may be flushed (group 0)
-    if (grp == 1) c.next(ntiles);
-    for (; c.n < nitems; c.next(ntiles), c.next(ntiles)) {
+    if (!kGdHalves && grp == 1) c.next(ntiles);
+    for (; c.n < nitems; c.next(ntiles)) {
       if (c.li != li_inv) {
         li_inv = c.li;
         const int sB = __ldg(&g.tc_meta[(l0 + c.li) * g.tc_nchunks + blockIdx.x].x);
@@ -287,8 +345,11 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
       }
       const int st = c.n % kTc2S, b = c.n % kGdBuf;
       const float* rec0 = reinterpret_cast<const float*>(smem + L::REC_OFF + b * L::REC);
+      if (q == 0 && lane == 0 && (!kGdHalves || grp == 0)) GD_STAMP(5, c.n);
       mbar_spin(sbar_s + 8u * st, (unsigned)(c.n / kTc2S) & 1u);
       tc_fence_after();
+      if (q == 0 && lane == 0 && (!kGdHalves || grp == 0)) GD_STAMP(0, c.n);
+      if (lane == 0 && (!kGdHalves || grp == 0)) GD_STAMP(10 + q, c.n);
       // UMMA 1 of this item follows UMMA 2 of item n - 3: the groups ending
       // there are final
       if (grp == 0)
@@ -297,7 +358,7 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
       mbar_spin(sbar_f + 8u * b, (unsigned)(c.n / kGdBuf) & 1u);  // records visible
       const unsigned long long ninv2 = f2pack(-inv, -inv);
 #pragma unroll 1
-      for (int h = 0; h < 2; ++h) {  // pixel halves [32 h, 32 h + 32)
+      for (int h = kGdHalves ? grp : 0; h < (kGdHalves ? grp + 1 : 2); ++h) {  // pixel halves [32 h, 32 h + 32)
         const unsigned ts = tmem + 64u * st + lane_off + 32u * h;
         const float* rec = rec0 + 32 * h;
         uint32_t sv[32];
@@ -307,55 +368,83 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
         const unsigned hit = __ballot_sync(0xffffffffu, (unsigned)(lab_x - g0w) < 32u);
         tmem_ld_wait();
         tmem_regs_ready(sv);
-        float rr[32];
-#pragma unroll
-        for (int x4 = 0; x4 < 32; x4 += 4) {
-          const float4 w4 = *reinterpret_cast<const float4*>(rec + x4);
-          const unsigned long long a01 =
-              ffma2(f2pack(__uint_as_float(sv[x4]), __uint_as_float(sv[x4 + 1])), ninv2, f2pack(w4.x, w4.y));
-          const unsigned long long a23 =
-              ffma2(f2pack(__uint_as_float(sv[x4 + 2]), __uint_as_float(sv[x4 + 3])), ninv2, f2pack(w4.z, w4.w));
-          rr[x4] = ex2_approx(f2lo(a01));  // p/2 * 2^13 = 2^(13 + w - h~'')
-          rr[x4 + 1] = ex2_approx(f2hi(a01));
-          rr[x4 + 2] = ex2_approx(f2lo(a23));
-          rr[x4 + 3] = ex2_approx(f2hi(a23));
-        }
-        if (hit) {  // label grain: -(1 - p_G)/2 * 2^13 from pass 1 (no cancellation)
-          // the pixels of each distinct in-range label at once (a 32-pixel run
-          // mostly lies in one grain): one round per distinct label, not per pixel
-          const unsigned same = __match_any_sync(0xffffffffu, lab_x);
-          unsigned mine = 0u;
-          for (unsigned m = hit; m;) {
-            const int x = __ffs(m) - 1;
-            const unsigned gx = __shfl_sync(0xffffffffu, same, x);
-            if (__shfl_sync(0xffffffffu, lab_x, x) == i) mine = gx;
-            m &= ~gx;
-          }
-          if (__any_sync(0xffffffffu, mine != 0u)) {
-            const float* qn = rec + 2 * kTc2Px;
-#pragma unroll
-            for (int x = 0; x < 32; ++x)
-              if (mine & (1u << x)) rr[x] = qn[x];
-          }
-        }
-        // exact split: hi = rr with the 13 low mantissa bits cleared (an fp16
-        // value), lo = rr - hi (exact in fp32, |lo| < 2^-10 |rr|) rounded to fp16
         uint32_t pp[32];  // [0, 16): r'_hi pairs, [16, 32): r'_lo pairs
+        // exact split: hi = r' with the 13 low mantissa bits cleared (an fp16
+        // value), lo = r' - hi (exact in fp32, |lo| < 2^-10 |r'|) rounded to fp16
+        if (PGX_GD_ILV && !hit) {
+          // software-pipelined by pixel pairs: exponentials of pair cc, split and
+          // conversions of pair cc - LAG
+          constexpr int LAG = 3;
+          float ra[16], rb[16];
 #pragma unroll
-        for (int cc = 0; cc < 16; ++cc) {
-          const float h0 = __uint_as_float(__float_as_uint(rr[2 * cc]) & 0xffffe000u);
-          const float h1 = __uint_as_float(__float_as_uint(rr[2 * cc + 1]) & 0xffffe000u);
-          const unsigned long long lo2 =
-              ffma2(f2pack(h0, h1), f2pack(-1.0f, -1.0f), f2pack(rr[2 * cc], rr[2 * cc + 1]));
-          pp[cc] = pack_h2(h0, h1);
-          pp[16 + cc] = pack_h2(f2lo(lo2), f2hi(lo2));
+          for (int cc = 0; cc < 16 + LAG; ++cc) {
+            if (cc < 16) {
+              const float2 w2 = *reinterpret_cast<const float2*>(rec + 2 * cc);
+              const unsigned long long a01 = ffma2(
+                  f2pack(__uint_as_float(sv[2 * cc]), __uint_as_float(sv[2 * cc + 1])), ninv2, f2pack(w2.x, w2.y));
+              ra[cc] = ex2_ordered(f2lo(a01));  // p/2 * 2^13 = 2^(13 + w - h~'')
+              rb[cc] = ex2_ordered(f2hi(a01));
+            }
+            if (cc >= LAG) {
+              const int c2 = cc - LAG;
+              const float h0 = __uint_as_float(__float_as_uint(ra[c2]) & 0xffffe000u);
+              const float h1 = __uint_as_float(__float_as_uint(rb[c2]) & 0xffffe000u);
+              const unsigned long long lo2 = ffma2(f2pack(h0, h1), f2pack(-1.0f, -1.0f), f2pack(ra[c2], rb[c2]));
+              pp[c2] = pack_h2_ordered(h0, h1);
+              pp[16 + c2] = pack_h2_ordered(f2lo(lo2), f2hi(lo2));
+            }
+          }
+        } else {
+          float rr[32];
+#pragma unroll
+          for (int x4 = 0; x4 < 32; x4 += 4) {
+            const float4 w4 = *reinterpret_cast<const float4*>(rec + x4);
+            const unsigned long long a01 =
+                ffma2(f2pack(__uint_as_float(sv[x4]), __uint_as_float(sv[x4 + 1])), ninv2, f2pack(w4.x, w4.y));
+            const unsigned long long a23 =
+                ffma2(f2pack(__uint_as_float(sv[x4 + 2]), __uint_as_float(sv[x4 + 3])), ninv2, f2pack(w4.z, w4.w));
+            rr[x4] = ex2_approx(f2lo(a01));  // p/2 * 2^13 = 2^(13 + w - h~'')
+            rr[x4 + 1] = ex2_approx(f2hi(a01));
+            rr[x4 + 2] = ex2_approx(f2lo(a23));
+            rr[x4 + 3] = ex2_approx(f2hi(a23));
+          }
+          if (hit) {  // label grain: -(1 - p_G)/2 * 2^13 from pass 1 (no cancellation)
+            // the pixels of each distinct in-range label at once (a 32-pixel run
+            // mostly lies in one grain): one round per distinct label, not per pixel
+            const unsigned same = __match_any_sync(0xffffffffu, lab_x);
+            unsigned mine = 0u;
+            for (unsigned m = hit; m;) {
+              const int x = __ffs(m) - 1;
+              const unsigned gx = __shfl_sync(0xffffffffu, same, x);
+              if (__shfl_sync(0xffffffffu, lab_x, x) == i) mine = gx;
+              m &= ~gx;
+            }
+            if (__any_sync(0xffffffffu, mine != 0u)) {
+              const float* qn = rec + 2 * kTc2Px;
+#pragma unroll
+              for (int x = 0; x < 32; ++x)
+                if (mine & (1u << x)) rr[x] = qn[x];
+            }
+          }
+#pragma unroll
+          for (int cc = 0; cc < 16; ++cc) {
+            const float h0 = __uint_as_float(__float_as_uint(rr[2 * cc]) & 0xffffe000u);
+            const float h1 = __uint_as_float(__float_as_uint(rr[2 * cc + 1]) & 0xffffe000u);
+            const unsigned long long lo2 =
+                ffma2(f2pack(h0, h1), f2pack(-1.0f, -1.0f), f2pack(rr[2 * cc], rr[2 * cc + 1]));
+            pp[cc] = pack_h2(h0, h1);
+            pp[16 + cc] = pack_h2(f2lo(lo2), f2hi(lo2));
+          }
         }
         tmem_st32(ts, pp);
       }
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
+      if (q == 0 && lane == 0 && (!kGdHalves || grp == 0)) GD_STAMP(1, c.n);
+      if (lane == 0 && (!kGdHalves || grp == 0)) GD_STAMP(6 + q, c.n);
       if (lane == 0) mbar_arrive(&bar_p[st]);
+      if (!kGdHalves) c.next(ntiles);
     }
     // the last groups: complete once the final commit lands
     if (grp == 0) {

@@ -19,7 +19,7 @@ $CMD > $OUT/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/${TAG}_${CFG}_${PREC}_launches.csv $CMD > $OUT/ncu_launch.log 2>&1
 python tools/run_eval.py --config $CFG --precision $PREC --iters 2 > $OUT/plain2.log 2>&1 && \
-ncu -f --set full --clock-control none --import-source on -k regex:"sweep|grad|pass1|pass2|tail" -s 3 -c 3 \
+ncu -f --set full --clock-control none --import-source on -k regex:"tc_sweep|tc_grad|tc_coeffs" -s 3 -c 3 \
     -o /tmp/prof_${TAG}_${CFG}_${PREC} python tools/run_eval.py --config $CFG --precision $PREC --iters 2 > $OUT/ncu_full.log 2>&1
 python3 tools/ncu_summary.py /tmp/prof_${TAG}_${CFG}_${PREC}.ncu-rep > $OUT/${TAG}_${CFG}_${PREC}_ncu_summary.txt 2>&1
 ncu -i /tmp/prof_${TAG}_${CFG}_${PREC}.ncu-rep --page raw --csv > /tmp/raw.csv 2>&1
