@@ -49,7 +49,7 @@ constexpr int kGdThreads = kTc2Epi + 64;  // + MMA warp + loader warp
 // lane quarter x pixel half), so two finished S stages always wait ahead of
 // the epilogue; false = two groups of 4 warps on alternate items
 #ifndef PGX_GD_HALVES
-#define PGX_GD_HALVES 1
+#define PGX_GD_HALVES 0
 #endif
 constexpr bool kGdHalves = PGX_GD_HALVES != 0;
 #ifdef PGX_GD_TRACE
@@ -201,31 +201,28 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
     // ======================= loader warp: every image and every item's pixel
     // operands + records, in consumption order; a buffer is refilled once the
     // MMAs that read it are complete (commits of the MMA warp)
-    Cur cl{0, 0, t0};
-    int al = 0;  // lines whose coefficient image has been requested
-    for (; cl.n < nitems; cl.next(ntiles)) {
-      if (cl.n == 0 || cl.t == 0) {  // the line's image (lines ahead as the slots free up)
-        for (; al <= cl.li && al < nlines; ++al) {
-          const int ab = al % kGdA;
-          if (al >= kGdA) mbar_wait_sleep(&bar_af[ab], (unsigned)((al - kGdA) / kGdA) & 1u);
-          if (lane == 0) {
+    if (elect_one()) {
+      Cur cl{0, 0, t0};
+      int al = 0;  // lines whose coefficient image has been requested
+      for (; cl.n < nitems; cl.next(ntiles)) {
+        if (cl.n == 0 || cl.t == 0) {  // the line's image (lines ahead as the slots free up)
+          for (; al <= cl.li && al < nlines; ++al) {
+            const int ab = al % kGdA;
+            if (al >= kGdA) mbar_wait_sleep(&bar_af[ab], (unsigned)((al - kGdA) / kGdA) & 1u);
             mbar_arrive_expect_tx(&bar_a[ab], L::A1);
             bulk_g2s(smem + L::A1_OFF + ab * L::A1,
                      g.tc_img + ((l0 + al) * g.tc_nchunks + blockIdx.x) * (int64_t)L::A1, L::A1, &bar_a[ab]);
           }
-          __syncwarp();
         }
-      }
-      const int b = cl.n % kGdBuf;
-      if (cl.n >= kGdBuf) mbar_wait_sleep(&bar_pf[b], (unsigned)((cl.n - kGdBuf) / kGdBuf) & 1u);
-      if (lane == 0) {
+        const int b = cl.n % kGdBuf;
+        if (cl.n >= kGdBuf) mbar_wait_sleep(&bar_pf[b], (unsigned)((cl.n - kGdBuf) / kGdBuf) & 1u);
         mbar_arrive_expect_tx(&bar_full[b], L::PIX + L::REC);
         bulk_g2s(smem + L::PIX_OFF + b * L::PIX, g.tc_pix + (int64_t)cl.t * L::PIX, L::PIX, &bar_full[b]);
         bulk_g2s(smem + L::REC_OFF + b * L::REC,
                  g.tc_rec + ((l0 + cl.li) * ntiles + cl.t) * (int64_t)kTc2RecFloats, L::REC, &bar_full[b]);
       }
-      __syncwarp();
     }
+    __syncwarp();
   } else if (warp == kGdMmaWarp) {
     // ======================= MMA issuer: ONE thread runs the whole role (no
     // warp-level re-convergence inside the loop), and every tcgen05 operand is

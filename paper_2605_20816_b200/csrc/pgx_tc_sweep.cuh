@@ -48,6 +48,11 @@ constexpr int kSwCols = 64;                      // grains per MMA block (UMMA N
 constexpr int kSwBufs = 2;                       // accumulators per slot
 constexpr int kSwRingMax = 16;                   // coefficient images in flight
 constexpr float kSwStale = 24.0f;                // ref may lag the min by this (log2 units)
+// pairs (of the 16 per 32-column block) whose exponentials run on the FMA pipe
+// (pexp2) instead of MUFU: the sweep is MUFU bound
+#ifndef PGX_SW_POLY
+#define PGX_SW_POLY 2
+#endif
 
 template <int J>
 struct SwSmem {
@@ -297,7 +302,9 @@ __global__ void __launch_bounds__(kSwThreads, 1) k_tc_sweep(GridParams g) {
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
             const unsigned long long a = ffma2(f2pack(w[e], w[e + 1]), ninv2, ref2);
-            const unsigned long long y = f2pack(ex2_approx(f2lo(a)), ex2_approx(f2hi(a)));
+            // (every (16 / PGX_SW_POLY)-th pair on the FMA pipe)
+            const bool poly = PGX_SW_POLY > 0 && (e / 2) % (16 / (PGX_SW_POLY > 0 ? PGX_SW_POLY : 1)) == 1;
+            const unsigned long long y = poly ? pexp2(a) : f2pack(ex2_approx(f2lo(a)), ex2_approx(f2hi(a)));
             if (e & 2)
               sb = fadd2(sb, y);
             else
