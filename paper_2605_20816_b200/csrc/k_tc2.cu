@@ -16,7 +16,7 @@ void tc_dispatch_coeffs(const GridParams& g, const GridPlan& gp, cudaStream_t s)
 
 template <int DIM, int D>
 void tc_dispatch_pix(const GridParams& g, const GridPlan& gp, cudaStream_t s) {
-  k_tc_pix<D><<<g.side / kTcPixTile, kTcPixTile, 0, s>>>(g.M, g.legendre, gp.tc_pix);
+  k_tc_pix<D><<<g.pside / kTcPixTile, kTcPixTile, 0, s>>>(g.M, g.legendre, gp.tc_pix);
 }
 
 template <int DIM, int D>

@@ -695,18 +695,34 @@ pgx_status pgx_assign(pgx_problem* pb, const void* theta, uint32_t flags, int64_
   prm.theta = theta64;
   prm.labels_out = reinterpret_cast<long long*>(dev ? labels_out : (int64_t*)pb->d_labels_out);
   prm.margin_out = margin_out ? (dev ? margin_out : pb->d_margin_out) : nullptr;
-  if (pb->d_design)
+  // tensor-core problems assign with the sweep kernel's ASSIGN variant (fp32
+  // screening on the tensor cores, exact fp64 decision of every candidate, the
+  // tail's exact re-scan for the rest): bit-identical labels, no N x P costs
+  const bool use_tc = pb->grid.enabled && pb->grid.tc && !pb->d_design;
+  int blocks1 = pb->blocks1;
+  pb->prof_reset();
+  if (use_tc) {
+    GridProf prof{pb, [](void* c, const char* n) { static_cast<pgx_problem*>(c)->prof_begin(n); },
+                  [](void* c) { static_cast<pgx_problem*>(c)->prof_end(); }};
+    st = grid_assign(pb->grid, prm, s, &launches, &blocks1, prof);
+    if (st != PGX_OK) return fail(st, "grid assign: %s", cudaGetErrorString(cudaGetLastError()));
+  } else if (pb->d_design) {
     launch_design_pass1(prm, pb->d_design, pb->K, pb->blocks1, false, s);
-  else
+    ++launches;
+  } else {
+    pb->prof_begin("general_assign");
     PGX_DISPATCH(launch_general_pass1, prm, pb->blocks1, false, s);
+    pb->prof_end();
+    ++launches;
+  }
   PGX_LAUNCH_CHECK();
-  ++launches;
   TailParams tp{};
   tp.want_grad = 0;
+  tp.fix_amb = use_tc ? 1 : 0;
   tp.ticket = reinterpret_cast<unsigned*>(pb->d_counters + 2);
   tp.part_th2 = pb->d_part_th2;
   FinalParams& fp = tp.fin;
-  fp.blocks1 = pb->blocks1;
+  fp.blocks1 = blocks1;
   fp.K = pb->K;
   fp.N = pb->N;
   fp.P = pb->P;

@@ -17,6 +17,7 @@ struct GridPlan {
   bool enabled = false;
   bool tc = false;  // PGX_PREC_TC: tensor-core pass 1
   int dim = 2, D = 1;
+  int pside = 0;    // tensor-core tiles: side rounded up to a multiple of 128
   int R = 1, segs = 1, lines = 0, blocks1 = 0;
   int tc_blocks = 0;
   int tc2_gtiles = 0, tc2_lps = 1, tc2_splits = 0;  // tensor-core pass 2 (0 = CUDA-core pass 2)
@@ -85,28 +86,31 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
   gp.enabled = false;
   if (d->resolution <= 0 || d->precision == PGX_PREC_EXACT) return;
   const int side = 2 * d->resolution;
-  if (side % 128 != 0) return;  // small grids use the general path
+  // the fp64 separable kernels need side % 128 == 0; the tensor-core kernels
+  // pad any side >= 64 to the next multiple of 128 (masked pixels); smaller
+  // grids use the general path
+  const bool tc_ok = d->precision == PGX_PREC_TC && side >= 64 && (d->n_grains + 127) / 128 <= 65535;
+  if (side % 128 != 0 && !tc_ok) return;
   if (d->dim == 2 && d->degree > 8) return;
   if (d->dim == 3 && d->degree > 4) return;
   gp.enabled = true;
   gp.dim = d->dim;
   gp.D = d->degree;
   gp.lines = (int)(d->n_points / side);
+  gp.pside = (side + 127) / 128 * 128;
   // pixels per thread: register blocking of the shared B'' loads, bounded by
   // the register file and by the wave count (>= ~6 CTAs per SM when possible)
   const int rmax = d->degree <= 3 ? 4 : (d->degree <= 5 ? 2 : 1);
-  int R = std::min(rmax, side / 128);
+  int R = std::max(1, std::min(rmax, side / 128));
   while (R > 1 && (int64_t)gp.lines * (side / (128 * R)) < 6 * sms) R /= 2;
   gp.R = R;
-  gp.segs = side / (128 * gp.R);
+  gp.segs = std::max(1, side / (128 * gp.R));
   gp.blocks1 = gp.lines * gp.segs;
-  // tensor-core pass 1: <= 2 CTAs per SM (256 TMEM columns each); R tiles of
-  // 128 pixels share each chunk's coefficient build
   // (k_tc_coeffs puts the 128-grain chunks on gridDim.y)
-  gp.tc = d->precision == PGX_PREC_TC && (d->n_grains + 127) / 128 <= 65535;
+  gp.tc = tc_ok;
   if (gp.tc) {
     // tensor-core pass 1 (k_tc_sweep): persistent, one CTA per SM, items of 4 tiles
-    const int64_t ntiles = (int64_t)gp.lines * (side / kTcThreadsTile);
+    const int64_t ntiles = (int64_t)gp.lines * (gp.pside / kTcThreadsTile);
     gp.tc_blocks = (int)std::min<int64_t>((ntiles + 3) / 4, (int64_t)sms);
     gp.blocks1 = gp.tc_blocks;
   }
@@ -132,7 +136,7 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
   gp.smem2 = K * kG2Threads * 8;
   // (>= 2 tiles per line: two consecutive one-item R groups would reuse an
   // accumulator before its flush)
-  if (gp.tc && side % kTc2Px == 0 && side >= 2 * kTc2Px) {
+  if (gp.tc) {  // (pside >= 128: at least two 64-pixel tiles per line)
     // tensor-core pass 2: 128-grain tiles x line ranges, 2 CTAs per SM; the
     // split count minimises waves x lines-per-CTA (ties: fewer splits, so the
     // tail reduces less)
@@ -140,7 +144,7 @@ inline void grid_plan_shape(GridPlan& gp, const pgx_desc* d, int sms) {
     // line-aligned CTA ranges unless item-granular ones are >= 5% cheaper
     // (c2: 28 items per CTA instead of 4 lines = 32; the mid-line kernel
     // variant costs registers, measured 3% slower per item at c5)
-    const int tpl2 = side / kTc2Px;
+    const int tpl2 = gp.pside / kTc2Px;
     tc2_splits_for(gp.lines, gp.tc2_gtiles, 2LL * sms, 8 * sms, gp.tc2_lps, gp.tc2_splits);
     int64_t ips = 0;
     int isp = 0;
@@ -174,7 +178,9 @@ inline GridBytes grid_bytes(const GridPlan& gp, const pgx_desc* d) {
   if (!gp.enabled) return b;
   const int K = feature_count(d->dim, d->degree);
   b.part = (size_t)std::max(gp.splits, gp.part_splits) * K * d->n_grains;
-  b.main = b.part * 8 + (size_t)d->n_points * 16 + 256;
+  // per-pixel scratch, 16 B per pixel (tensor-core problems: per padded pixel, the pass-2 records)
+  const size_t npix = gp.tc ? (size_t)gp.lines * gp.pside : (size_t)d->n_points;
+  b.main = b.part * 8 + npix * 16 + 256;
   if (gp.tc) {
     const int J = d->degree + 1;
     const size_t nchunks = (d->n_grains + kTcCoefChunk - 1) / kTcCoefChunk;
@@ -184,7 +190,7 @@ inline GridBytes grid_bytes(const GridPlan& gp, const pgx_desc* d) {
     b.nlc = (size_t)gp.lines * K;
     b.tc = b.ncoef * 8 + b.nimg + b.nmeta * 8 + b.nlc * 8 + 256;
     if (gp.tc2_splits > 0)
-      b.pix = (size_t)(2 * d->resolution / kTcPixTile) *
+      b.pix = (size_t)(gp.pside / kTcPixTile) *
               (tc_ksteps(J) * kTcPixTile * 32 + 2 * (kTcPixTile / 16) * 16 * 32);
   }
   return b;
@@ -205,7 +211,7 @@ inline cudaError_t grid_plan_create(GridPlan& gp, const pgx_desc* d, int sms, si
   bytes += b.main;
   gp.part_out = static_cast<double*>(gp.d_part);
   gp.pix_w = gp.part_out + b.part;
-  gp.pix_q = reinterpret_cast<float*>(gp.pix_w + d->n_points);
+  gp.pix_q = reinterpret_cast<float*>(gp.pix_w + (gp.tc ? (size_t)gp.lines * gp.pside : (size_t)d->n_points));
   if (gp.tc) {
     gp.tc_nchunks = (d->n_grains + kTcCoefChunk - 1) / kTcCoefChunk;
     e = cudaMalloc(&gp.d_tc, b.tc);

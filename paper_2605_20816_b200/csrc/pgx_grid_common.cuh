@@ -78,6 +78,7 @@ struct GridParams {
   int N;
   int M;           // resolution; side = 2M
   int side;
+  int pside;       // tensor-core kernels: side rounded up to a multiple of 128 (padding pixels masked)
   int legendre;
   int R;           // pixels per thread (pass 1)
   int lines;       // number of lines along the fast axis
@@ -117,8 +118,11 @@ struct GridParams {
   int part_off;                 // pass 1: first per-CTA partial slot
   int64_t line_lo;              // pass 2: first line (g.lines = end line)
   int split_off;                // pass 2: first gradient-partial split slot
-  float* tc_rec;                // [lines][side / 64][4][64] pass-2 pixel records
+  float* tc_rec;                // [lines][pside / 64][4][64] pass-2 pixel records
                                 // (w13, wl13, qn, label) written by TC pass 1
+  // hard-assignment variant of the tensor-core sweep (pgx_assign)
+  long long* labels_out;        // 1-based arg-min labels
+  float* margin_out;            // top-2 margin (nullable)
 };
 
 // Per-line factors: lc[k] = prod over the non-fast axes of u_axis[alpha]

@@ -35,14 +35,14 @@ struct GridProf {
   void (*end)(void*);
 };
 
-inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool want_grad,
-                            cudaStream_t s, int* launches, int* blocks1, const GridProf& prof) {
-  (void)prec;
+// the kernels' view of one evaluation / assignment on the plan
+inline GridParams grid_params(const GridPlan& gp, const EvalParams& e, bool want_grad) {
   GridParams g{};
   g.P = e.P;
   g.N = e.N;
   g.M = e.M;
   g.side = 2 * e.M;
+  g.pside = gp.pside;
   g.legendre = e.legendre;
   g.R = gp.R;
   g.lines = gp.lines;
@@ -73,10 +73,44 @@ inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool wa
   g.tc_lc = gp.tc_lc;
   g.tc_rec = want_grad ? gp.tc_rec : nullptr;
   g.tile_lo = 0;
-  g.tile_hi = (int64_t)gp.lines * (g.side / kTcThreadsTile);
+  g.tile_hi = (int64_t)gp.lines * (g.pside / kTcThreadsTile);
   g.part_off = 0;
   g.line_lo = 0;
   g.split_off = 0;
+  g.labels_out = e.labels_out;
+  g.margin_out = e.margin_out;
+  return g;
+}
+
+// hard assignment on the tensor-core path: coefficient tables + the ASSIGN sweep
+inline pgx_status grid_assign(GridPlan& gp, const EvalParams& e, cudaStream_t s, int* launches,
+                              int* blocks1, const GridProf& prof) {
+  GridParams g = grid_params(gp, e, false);
+  prof.begin(prof.ctx, "tc_coeffs");
+  if (gp.dim == 2) {
+    PGX_GRID_DEG(2, tc_dispatch_coeffs, g, gp, s)
+  } else {
+    PGX_GRID_DEG3(tc_dispatch_coeffs, g, gp, s)
+  }
+  prof.end(prof.ctx);
+  ++*launches;
+  if (cudaPeekAtLastError() != cudaSuccess) return PGX_ERR_CUDA;
+  prof.begin(prof.ctx, "tc_assign");
+  if (gp.dim == 2) {
+    PGX_GRID_DEG(2, tc_dispatch_assign, g, gp.tc_blocks, s)
+  } else {
+    PGX_GRID_DEG3(tc_dispatch_assign, g, gp.tc_blocks, s)
+  }
+  prof.end(prof.ctx);
+  ++*launches;
+  *blocks1 = gp.tc_blocks;
+  return cudaPeekAtLastError() == cudaSuccess ? PGX_OK : PGX_ERR_CUDA;
+}
+
+inline pgx_status grid_eval(GridPlan& gp, const EvalParams& e, int prec, bool want_grad,
+                            cudaStream_t s, int* launches, int* blocks1, const GridProf& prof) {
+  (void)prec;
+  GridParams g = grid_params(gp, e, want_grad);
   if (gp.tc && gp.tc_pix && !gp.tc_pix_ready) {  // once per problem
     if (gp.dim == 2) {
       PGX_GRID_DEG(2, tc_dispatch_pix, g, gp, s)

@@ -103,6 +103,8 @@ void tc_dispatch_pix(const GridParams& g, const GridPlan& gp, cudaStream_t s);
 template <int DIM, int D>
 void tc_dispatch_pass1(const GridParams& g, int blocks, cudaStream_t s);
 template <int DIM, int D>
+void tc_dispatch_assign(const GridParams& g, int blocks, cudaStream_t s);
+template <int DIM, int D>
 void tc_dispatch_pass2(const GridParams& g, dim3 grid, cudaStream_t s);
 
 }  // namespace pgx

@@ -143,8 +143,9 @@ __global__ void __launch_bounds__(kTcPixTile) k_tc_pix(int M, int legendre,
   double u[J];
   axis_table<D>(axis_coord(col, M), legendre != 0, u);
   __half hi[J], lo[J];
+  // (padding columns of a side % 128 != 0 grid: zero operands, so S = 0 and R += 0)
 #pragma unroll
-  for (int j = 0; j < J; ++j) split_f16(u[j] * 1024.0, hi[j], lo[j]);
+  for (int j = 0; j < J; ++j) split_f16(col < 2 * M ? u[j] * 1024.0 : 0.0, hi[j], lo[j]);
 #pragma unroll
   for (int s = 0; s < KS; ++s) {
     __half row[16];

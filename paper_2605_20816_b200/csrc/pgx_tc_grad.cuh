@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gbase = blockIdx.x * kTc2Grains;
   // items (line, tile) of this CTA: [a0, a1) of the launch's line range
-  const int ntiles = g.side / kTc2Px;
+  const int ntiles = g.pside / kTc2Px;
   const int gpl = (ntiles + kTc2Group - 1) / kTc2Group;  // R groups per line
   const int64_t a0 = g.line_lo * ntiles + (int64_t)blockIdx.y * g.items_per_split;
   const int64_t a1 = min((int64_t)g.lines * ntiles, a0 + g.items_per_split);

@@ -66,7 +66,13 @@ struct SwSmem {
   static constexpr int TOTAL = IMG_OFF + RING * IMG;
 };
 
-template <int DIM, int D>
+// ASSIGN: the hard-assignment variant (pgx_assign; objective.py:62-77): the
+// same sweep without exponentials, label term or pass-2 records; it writes the
+// 1-based arg-min label and the top-2 margin per pixel.
+// Sides that are not a multiple of 128 run on tiles padded to g.pside: the
+// padding pixels ride through the MMAs and barriers, contribute nothing and
+// get an all-zero (-inf exponent) pass-2 record.
+template <int DIM, int D, bool ASSIGN>
 __global__ void __launch_bounds__(kSwThreads, 1) k_tc_sweep(GridParams g) {
   constexpr int J = D + 1;
   using L = SwSmem<J>;
@@ -85,7 +91,7 @@ __global__ void __launch_bounds__(kSwThreads, 1) k_tc_sweep(GridParams g) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int N = g.N;
   const double c = g.c;
-  const int tpl = g.side / kTcThreadsTile;  // tiles per line
+  const int tpl = g.pside / kTcThreadsTile;  // tiles per (padded) line
   const int64_t ntiles = (int64_t)g.lines * tpl;
   const int64_t nitems = (ntiles + kSwSlots - 1) / kSwSlots;
   const int nimg = (N + kTcCoefChunk - 1) / kTcCoefChunk;
@@ -218,7 +224,7 @@ __global__ void __launch_bounds__(kSwThreads, 1) k_tc_sweep(GridParams g) {
       axis_table<D>(axis_coord(col, g.M), g.legendre != 0, u);
       __half hi[J], lo[J];
 #pragma unroll
-      for (int j = 0; j < J; ++j) split_f16(u[j] * 1024.0, hi[j], lo[j]);
+      for (int j = 0; j < J; ++j) split_f16(col < g.side ? u[j] * 1024.0 : 0.0, hi[j], lo[j]);  // padding: 0
       unsigned char* A_s = smem + L::A_OFF + (ib * kSwSlots + s) * L::A_TILE;
 #pragma unroll
       for (int k = 0; k < 16 * KS; ++k) {
@@ -239,14 +245,17 @@ __global__ void __launch_bounds__(kSwThreads, 1) k_tc_sweep(GridParams g) {
       if (tile >= ntiles) continue;  // (only in a CTA's last item; no MMA is issued for it)
       const int64_t line = tile / tpl;
       const int col = (int)(tile % tpl) * kTcThreadsTile + prow;
+      const bool valid = col < g.side;  // (false on the padding of a side % 128 != 0 grid)
       const int64_t p = line * g.side + col;
-      const int lab = g.labels[p];
+      const int lab = valid && g.labels ? g.labels[p] : -1;
       const double* coef_line = g.tc_coef + line * (int64_t)N * J;
       const int2* meta = g.tc_meta + line * g.tc_nchunks;
       float ref = CUDART_INF_F, m1 = CUDART_INF_F, m2b = CUDART_INF_F, m3b = CUDART_INF_F, bmax = 0.0f;
       int b1 = 0, b2 = 0;
       unsigned mask1 = 0u, mask2 = 0u;  // columns of 32-blocks b1, b2 within the candidate window
       float sx = 0.0f, sxc = 0.0f;      // Kahan-compensated sum of the 32-block sums
+      float gm1 = CUDART_INF_F, gm2 = CUDART_INF_F;  // ASSIGN + margins: two smallest logits (fp32)
+      const bool want_margin = ASSIGN && g.margin_out != nullptr;
       float inv = 0.0f, rinv = 0.0f, dblk = 0.0f;
       const float bandf = (float)(c * fmax(kTieRtol, g.tau_amb)), inv_cf = (float)(1.0 / c);
 
@@ -260,6 +269,18 @@ __global__ void __launch_bounds__(kSwThreads, 1) k_tc_sweep(GridParams g) {
         const float mb = fminf(fminf(fminf(t11[0], fminf(t11[1], t11[2])), fminf(t11[3], fminf(t11[4], t11[5]))),
                                fminf(fminf(t11[6], fminf(t11[7], t11[8])), fminf(t11[9], t11[10])));
         const float mbs = mb * inv;
+        if (ASSIGN && want_margin) {  // runner-up for the reported margin: the block's two smallest
+          float a = CUDART_INF_F, b = CUDART_INF_F;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float t = fmaxf(a, w[e]);
+            a = fminf(a, w[e]);
+            b = fminf(b, t);
+          }
+          const float a1 = a * inv, a2 = b * inv;
+          gm2 = fminf(fmaxf(gm1, a1), fminf(gm2, a2));
+          gm1 = fminf(gm1, a1);
+        }
         if (mbs < m3b) {  // top-3 blocks (rare after the first few)
           if (mbs < m2b) {
             // candidate columns: within 2 delta + tie band of the block min; bit e =
@@ -293,40 +314,42 @@ __global__ void __launch_bounds__(kSwThreads, 1) k_tc_sweep(GridParams g) {
             ref = nref;
           }
         }
-        const unsigned long long ninv2 = f2pack(-inv, -inv), ref2 = f2pack(ref, ref);
-        unsigned long long sa = 0ull, sb = 0ull;
-        const int labc = lab - kb * 32;
-        // padding columns (+inf) give exact zeros: only a block holding some
-        // lane's label column needs the masked loop
-        if (!__any_sync(0xffffffffu, (unsigned)labc < 32u)) {
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const unsigned long long a = ffma2(f2pack(w[e], w[e + 1]), ninv2, ref2);
-            // (every (16 / PGX_SW_POLY)-th pair on the FMA pipe)
-            const bool poly = PGX_SW_POLY > 0 && (e / 2) % (16 / (PGX_SW_POLY > 0 ? PGX_SW_POLY : 1)) == 1;
-            const unsigned long long y = poly ? pexp2(a) : f2pack(ex2_approx(f2lo(a)), ex2_approx(f2hi(a)));
-            if (e & 2)
-              sb = fadd2(sb, y);
-            else
-              sa = fadd2(sa, y);
+        if constexpr (!ASSIGN) {
+          const unsigned long long ninv2 = f2pack(-inv, -inv), ref2 = f2pack(ref, ref);
+          unsigned long long sa = 0ull, sb = 0ull;
+          const int labc = lab - kb * 32;
+          // padding columns (+inf) give exact zeros: only a block holding some
+          // lane's label column needs the masked loop
+          if (!__any_sync(0xffffffffu, (unsigned)labc < 32u)) {
+  #pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              const unsigned long long a = ffma2(f2pack(w[e], w[e + 1]), ninv2, ref2);
+              // (every (16 / PGX_SW_POLY)-th pair on the FMA pipe)
+              const bool poly = PGX_SW_POLY > 0 && (e / 2) % (16 / (PGX_SW_POLY > 0 ? PGX_SW_POLY : 1)) == 1;
+              const unsigned long long y = poly ? pexp2(a) : f2pack(ex2_approx(f2lo(a)), ex2_approx(f2hi(a)));
+              if (e & 2)
+                sb = fadd2(sb, y);
+              else
+                sa = fadd2(sa, y);
+            }
+          } else {
+  #pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              const unsigned long long a = ffma2(f2pack(w[e], w[e + 1]), ninv2, ref2);
+              const float y0 = ex2_approx(f2lo(a)), y1 = ex2_approx(f2hi(a));
+              const unsigned long long y = f2pack(e != labc ? y0 : 0.0f, e + 1 != labc ? y1 : 0.0f);
+              if (e & 2)
+                sb = fadd2(sb, y);
+              else
+                sa = fadd2(sa, y);
+            }
           }
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const unsigned long long a = ffma2(f2pack(w[e], w[e + 1]), ninv2, ref2);
-            const float y0 = ex2_approx(f2lo(a)), y1 = ex2_approx(f2hi(a));
-            const unsigned long long y = f2pack(e != labc ? y0 : 0.0f, e + 1 != labc ? y1 : 0.0f);
-            if (e & 2)
-              sb = fadd2(sb, y);
-            else
-              sa = fadd2(sa, y);
-          }
+          const unsigned long long s2 = fadd2(sa, sb);
+          const float y = (f2lo(s2) + f2hi(s2)) - sxc;  // Kahan step
+          const float t = sx + y;
+          sxc = (t - sx) - y;
+          sx = t;
         }
-        const unsigned long long s2 = fadd2(sa, sb);
-        const float y = (f2lo(s2) + f2hi(s2)) - sxc;  // Kahan step
-        const float t = sx + y;
-        sxc = (t - sx) - y;
-        sx = t;
       };
 
 #pragma unroll 1
@@ -376,6 +399,16 @@ __global__ void __launch_bounds__(kSwThreads, 1) k_tc_sweep(GridParams g) {
       }
 
       // ------------------------------------------------ per-pixel finish
+      if (!valid) {
+        if (!ASSIGN && g.tc_rec) {  // r' = 2^(-inf) = 0 for every grain, no label grain
+          float* rec = g.tc_rec + (line * (g.pside / kTcPixTile) + (col >> 6)) * (4 * kTcPixTile) + (col & 63);
+          rec[0] = -CUDART_INF_F;
+          rec[kTcPixTile] = 0.0f;
+          rec[2 * kTcPixTile] = 0.0f;
+          reinterpret_cast<int*>(rec)[3 * kTcPixTile] = -1;
+        }
+        continue;
+      }
       // |h~'' - h''| <= delta: fp16 split (2^-21 relative per operand pair) plus
       // the fp32 accumulation of 3J products; generous factor 2
       const float delta = 2.0f * (4.7683716e-07f + 3 * J * 5.9604645e-08f) * bmax + 1e-30f;
@@ -383,7 +416,6 @@ __global__ void __launch_bounds__(kSwThreads, 1) k_tc_sweep(GridParams g) {
       const float wnd = 2.0f * delta + (float)band * 1.001f + 1e-30f;
       double u[J];
       axis_table<D>(axis_coord(col, g.M), g.legendre != 0, u);
-      const double hG = eval_line<J>(coef_line + (int64_t)lab * J, u);
       TcRare st;
       st.m = CUDART_INF;
       st.m2 = CUDART_INF;
@@ -404,36 +436,55 @@ __global__ void __launch_bounds__(kSwThreads, 1) k_tc_sweep(GridParams g) {
           const int i = bh * 32 + __ffs(mk) - 1;
           tc_rare_update(st, i, eval_line<J>(coef_line + (int64_t)i * J, u), c);
         }
-      // a third block as close (or an overflowing candidate list): exact re-scan in the tail
-      const bool found = st.cnt > 0 && !(st.flags & 2) && !(m3b <= m1 + wnd);
+      // a third block as close (or an overflowing candidate list, or logits
+      // beyond the fp32 range): exact re-scan in the tail
+      const bool found = st.cnt > 0 && !(st.flags & 2) && !(m3b <= m1 + wnd) && bmax <= 3e38f;
+      const double m2x = st.m2;  // exact runner-up among the candidates (+inf: a single candidate)
       st.m2 = fmin(st.m2, (double)(two ? m3b : m2b) - (double)delta);  // out-of-block runner-up bound
-      const double refd = (double)ref;
-      const double aG = hG - refd;
-      const double eG = exp2(-aG);
-      const double sxd = (double)sx - (double)sxc;
-      const double sum = sxd + eG;
-      const double l2s = log2(sum);
-      const double l = (-aG - l2s) * 0.69314718055994530942;  // log p_G: objective.py:103-106
-      ell += l;
-      if (!isfinite(l) || !(bmax <= 3e38f)) nonfinite = 1;
-      if (g.tc_rec) {  // pass-2 record: p_i/2 * 2^13 = 2^(w13 + wl13 - h~''_i)
-        const double w13 = refd - 1.0 - l2s + 13.0;
-        const float wh = (float)w13;
-        float* rec = g.tc_rec + (line * (g.side / kTcPixTile) + (col >> 6)) * (4 * kTcPixTile) + (col & 63);
-        rec[0] = wh;
-        rec[kTcPixTile] = (float)(w13 - (double)wh);
-        rec[2 * kTcPixTile] = (float)(-4096.0 * sxd / sum);  // -(1 - p_G)/2 * 2^13
-        reinterpret_cast<int*>(rec)[3 * kTcPixTile] = lab;
-      }
-      const double m = st.cnt > 0 ? st.m : hG;
-      g.pix_m[p] = m / c;
-      e0 += (hG - m) / c;  // objective.py:119
-      if (!found) {
-        const int slot = atomicAdd(g.fix_count, 1);
-        g.fix_list[slot] = (int)p;
+      if constexpr (ASSIGN) {
+        // (without candidates the tail's re-scan only needs an upper bound of the min)
+        const double m = st.cnt > 0 ? st.m : (double)m1 + (double)delta;
+        g.pix_m[p] = m / c;
+        // exact when the runner-up is a candidate, else its fp32 logit (error <= delta)
+        if (g.margin_out) g.margin_out[p] = (float)(fmax(fmin(m2x, (double)gm2) - m, 0.0) / c);
+        if (!found) {
+          const int slot = atomicAdd(g.fix_count, 1);
+          g.fix_list[slot] = (int)p;
+        } else {
+          g.labels_out[p] = st.b0 + 1;
+          correct += (st.b0 == lab) ? 1 : 0;
+          amb += ((st.m2 - st.m) <= c * g.tau_amb * (1.0 + fabs(st.m / c))) ? 1 : 0;
+        }
       } else {
-        correct += (st.b0 == lab) ? 1 : 0;
-        amb += ((st.m2 - st.m) <= c * g.tau_amb * (1.0 + fabs(st.m / c))) ? 1 : 0;
+        const double hG = eval_line<J>(coef_line + (int64_t)lab * J, u);
+        const double refd = (double)ref;
+        const double aG = hG - refd;
+        const double eG = exp2(-aG);
+        const double sxd = (double)sx - (double)sxc;
+        const double sum = sxd + eG;
+        const double l2s = log2(sum);
+        const double l = (-aG - l2s) * 0.69314718055994530942;  // log p_G: objective.py:103-106
+        ell += l;
+        if (!isfinite(l) || !(bmax <= 3e38f)) nonfinite = 1;
+        if (g.tc_rec) {  // pass-2 record: p_i/2 * 2^13 = 2^(w13 + wl13 - h~''_i)
+          const double w13 = refd - 1.0 - l2s + 13.0;
+          const float wh = (float)w13;
+          float* rec = g.tc_rec + (line * (g.pside / kTcPixTile) + (col >> 6)) * (4 * kTcPixTile) + (col & 63);
+          rec[0] = wh;
+          rec[kTcPixTile] = (float)(w13 - (double)wh);
+          rec[2 * kTcPixTile] = (float)(-4096.0 * sxd / sum);  // -(1 - p_G)/2 * 2^13
+          reinterpret_cast<int*>(rec)[3 * kTcPixTile] = lab;
+        }
+        const double m = st.cnt > 0 ? st.m : hG;
+        g.pix_m[p] = m / c;
+        e0 += (hG - m) / c;  // objective.py:119
+        if (!found) {
+          const int slot = atomicAdd(g.fix_count, 1);
+          g.fix_list[slot] = (int)p;
+        } else {
+          correct += (st.b0 == lab) ? 1 : 0;
+          amb += ((st.m2 - st.m) <= c * g.tau_amb * (1.0 + fabs(st.m / c))) ? 1 : 0;
+        }
       }
     }
     // per-CTA partials: warp shuffle tree, then warps in fixed order

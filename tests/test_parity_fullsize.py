@@ -93,3 +93,73 @@ def test_grid_kernels_vs_oracle(name, prec):
         assert abs(res.err - ref.err) * npx <= st.n_ambiguous, (res.err, ref.err, st.n_ambiguous)
         assert res.e0 == pytest.approx(ref.e0, rel=1e-9, abs=1e-12)
     prob.close()
+
+
+# ---------------------------------------------------------------- tensor-core hard assignment
+@pytest.mark.parametrize("name", ["c3_full", "c5_shape", "c4_shape_d2", "c4_shape_d4"])
+def test_tc_assign_vs_oracle(name):
+    """pgx_assign on a tensor-core problem runs the sweep's ASSIGN variant
+    (objective.py:62-77 / geometry.py:201-210): labels bit-identical to the
+    oracle except at ambiguous pixels, and to the exact fp64 kernels everywhere."""
+    import paper_2605_20816_b200 as pgb
+
+    c, refs = _oracle(name)
+    grid = pgb.make_grid(c["m"], c["dim"])
+    prob = pgb.Problem(grid, "legendre", c["degree"], c["n"], c["labels0"], precision="tc")
+    exact = pgb.Problem(grid, "legendre", c["degree"], c["n"], c["labels0"], precision="exact")
+    pts = oracle.grid_points(c["m"], c["dim"])
+    for th in c["thetas"]:
+        prob.set_profiling(True)
+        lab, margin, n_amb = prob.assign(th, with_margin=True)
+        names = [n for n, _ in prob.profile()]
+        prob.set_profiling(False)
+        assert "tc_assign" in names and not any(n.startswith("general") for n in names), names
+        lab_x, margin_x, n_amb_x = exact.assign(th, with_margin=True)
+        assert np.array_equal(lab, lab_x)
+        assert n_amb == n_amb_x
+        # the margin is exact when the runner-up is a candidate of the fp64 decision, else
+        # its fp32 tensor-core logit: absolute error <= delta ~ 4e-6 max_i sum_k |theta_ki|
+        atol = 1e-5 * np.abs(th).sum(axis=0).max()
+        assert np.abs(margin - margin_x).max() <= atol, (np.abs(margin - margin_x).max(), atol)
+        sub = np.random.default_rng(5).choice(len(pts), 4096, replace=False)
+        ref_lab = oracle.hard_assign_points(th, "legendre", c["degree"], pts[sub])
+        assert np.array_equal(lab[sub], ref_lab)
+    prob.close()
+    exact.close()
+
+
+# ---------------------------------------------------------------- padded (side % 128 != 0) grids
+@pytest.mark.parametrize("dim,m,d,n,eps", [(2, 70, 2, 60, 0.02),    # the paper's 140 x 140 map
+                                            (2, 70, 8, 300, 0.01),   # d >= 6 pass-2 variant
+                                            (2, 100, 4, 257, 0.01),  # 200 x 200, N % 128 != 0
+                                            (2, 33, 3, 7, 0.05),     # 66 x 66: one padded tile per line
+                                            (3, 36, 2, 40, 0.02)])   # 72^3 voxels
+def test_tc_padded_grid_vs_oracle(dim, m, d, n, eps):
+    """Grids whose side is not a multiple of 128 run the tcgen05 kernels on
+    tiles padded with masked pixels (geometry.py:59-71 grids of any resolution)."""
+    import paper_2605_20816_b200 as pgb
+
+    rng = np.random.default_rng(1000 * dim + m)
+    k = oracle.feature_count(d, dim)
+    labels0 = _labels_from_diagram(rng, "legendre", d, dim, m, n)
+    pts = oracle.grid_points(m, dim)
+    prob = pgb.Problem(pgb.make_grid(m, dim), "legendre", d, n, labels0, precision="tc")
+    assert prob.kernel_path == "grid_tc"
+    tphi, tgrad = TOL["tc"]
+    for th in (0.01 * rng.normal(size=(k, n)), 0.5 * rng.normal(size=(k, n))):
+        ref = oracle.evaluate_problem(th, "legendre", d, pts, labels0, eps, want_grad=True,
+                                      want_assign=True, threads=THREADS)
+        res, st, names = prob.eval_kernels(th, eps, want_grad=True, want_assign=True)
+        assert "tc_pass1" in names and "tc_pass2" in names, names
+        assert not any(nm.startswith("general") for nm in names), names
+        assert abs(res.phi - ref.phi) <= tphi * (1 + abs(ref.phi)), (res.phi, ref.phi)
+        gerr = np.abs(res.grad - ref.grad).max() / np.abs(ref.grad).max()
+        assert gerr <= tgrad, gerr
+        assert abs(res.err - ref.err) * len(labels0) <= st.n_ambiguous
+        assert res.e0 == pytest.approx(ref.e0, rel=1e-9, abs=1e-12)
+        lab = prob.assign(th)
+        assert np.array_equal(lab, oracle.hard_assign_points(th, "legendre", d, pts))
+        # a second evaluation is bit-identical (fixed-order reductions)
+        res2, _ = prob.eval(th, eps, want_grad=True, want_assign=True)
+        assert res2.phi == res.phi and np.array_equal(res2.grad, res.grad)
+    prob.close()
