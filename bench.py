@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "paper140"])
     # tc: tcgen05 logits (3-product fp16 split, fp32 accumulate) -- the north-star
     # path, within the stated 1e-6 (phi) / 1e-5 (grad) tolerances; fp64 and exact
     # are the tighter modes
@@ -202,7 +202,7 @@ def run_reference(args):
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     from paper_2605_20816_b200 import configs
 
-    w = configs.make(args.config, labeler="host" if args.config in ("c1", "c2") else "gpu")
+    w = configs.make(args.config, labeler="host" if args.config in ("c1", "c2", "paper140") else "gpu")
     threads = os.cpu_count() or 1
     import numpy as np
 
@@ -387,7 +387,7 @@ def run_ours(args):
     import paper_2605_20816_b200 as pgb
     from paper_2605_20816_b200 import _lib, configs
 
-    w = configs.make(args.config, labeler="host" if args.config in ("c1", "c2") else "gpu")
+    w = configs.make(args.config, labeler="host" if args.config in ("c1", "c2", "paper140") else "gpu")
     stream = torch.cuda.Stream(device=dev)
     prob = pgb.Problem(w.grid, w.kind, w.degree, w.n_grains, w.labels0,
                        precision=args.precision, device=local, stream=stream.cuda_stream)
@@ -487,6 +487,26 @@ def run_ours(args):
                     "dtype": DTYPE[m], "phi": float(stats_d[0].item())}
         pm.close()
 
+    # ---- hard assignment (pgx_assign: hard_assign without the N x P costs), device-timed
+    assign = None
+    try:
+        lab_d = torch.empty(P, dtype=torch.int64, device=dev)
+
+        def step_a():
+            prob.assign_device(theta_d.data_ptr(), flags & _lib.PGX_THETA_F32, lab_d.data_ptr())
+
+        ms = time_mode(prob, step_a, flush, stream, max(3, args.steps // 4), 2, dev)
+        prob.set_profiling(True)
+        with torch.cuda.stream(stream):
+            step_a()
+            a_kern = {n: v for n, v in prob.profile()}
+        prob.set_profiling(False)
+        t_a = sum(ms) / 1e3 / len(ms)
+        assign = {"ms_per_step": 1e3 * t_a, "value": P * N / t_a, "unit": "logits/s",
+                  "kernels_ms": a_kern, "labels_checksum": int(lab_d.sum().item())}
+    except Exception as exc:  # noqa: BLE001
+        assign = {"error": repr(exc)}
+
     # ---- roofline (§8d, whole evaluation) + the dominant kernel
     peaks, peaks_kind = load_peaks()
     clocks = clk.summary()
@@ -533,6 +553,7 @@ def run_ours(args):
                                  "pinned host memory), then stream sync"},
             "roofline": roofline,
             "modes": modes,
+            "assign": assign,
             "cpu_baseline": cpu_baseline,
             "fit_c1_gpu": fit,
             "gpu_launches": launches,

@@ -38,6 +38,7 @@ from .objective import (
 )
 from .heuristics import MomentSummary, heuristic_theta, moments
 from .optimizer import FitConfig, FitReport, fit, init_zero, line_search
+from . import binio  # noqa: E402,F401  (binary sidecars of the grain-map / theta text formats)
 
 __version__ = "0.1.0"
 

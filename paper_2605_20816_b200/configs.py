@@ -278,7 +278,26 @@ def c5(labeler="gpu", seed=5):
                     "Legendre d=8 (K=45), eps=0.005, lam=1e-5", int(np.unique(labels).size))
 
 
-CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5}
+def paper140(labeler="host", seed=14):
+    """The shape of the paper's own reconstruction experiment (Fig. 4:
+    |Omega| = 19,600 = 140 x 140 pixels, N = 50 cells, 2nd-degree fit, eps = 0.01) on a
+    seeded synthetic anisotropic power diagram; a side that is not a multiple of 128."""
+    rng = np.random.default_rng(seed)
+    M, N = 70, 50
+    seeds = rng.uniform(-1.0, 1.0, (N, 2))
+    weights = rng.normal(0.0, 0.01, N)
+    s = _log_uniform(rng, 0.5, 2.0, (N, 2))
+    R = _rotation2(rng.uniform(0.0, math.pi, N))
+    A = np.einsum("nij,nj,nkj->nik", R, s, R)
+    labels = _assign(_apd_theta(seeds, weights, A), MONOMIAL, 2, 2, M, labeler)
+    th = _bench_theta(rng, 6, N, "f64")
+    return Workload("paper140", 2, M, N, LEGENDRE, 2, 0.01, 0.0, labels, th, "f64", make_grid(M),
+                    "2D 140x140 (|Omega| = 19,600), anisotropic power diagram N=50, Legendre d=2 "
+                    "(K=6), eps=0.01 (the paper's reconstruction experiment shape)",
+                    int(np.unique(labels).size))
+
+
+CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5, "paper140": paper140}
 
 
 def make(name: str, labeler: str | None = None) -> Workload:

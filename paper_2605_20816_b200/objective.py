@@ -283,6 +283,12 @@ class Problem:
         _lib.check(self._lib.pgx_eval(self._h, theta_ptr, float(eps), float(lam),
                                       int(flags) | _lib.PGX_DEVICE_PTRS, grad_ptr, stats_ptr))
 
+    def assign_device(self, theta_ptr: int, flags: int, labels_ptr: int, margin_ptr: int = 0,
+                      stats_ptr: int = 0) -> None:
+        """Asynchronous hard assignment on device pointers (int64 labels, 1-based)."""
+        _lib.check(self._lib.pgx_assign(self._h, theta_ptr, int(flags) | _lib.PGX_DEVICE_PTRS,
+                                        labels_ptr, margin_ptr or None, stats_ptr or None))
+
     def soft_assign(self, theta, eps: float) -> np.ndarray:
         """Dense (N, P) softmax memberships (objective.py:80-87), pgx_soft_assign."""
         if not eps > 0:
@@ -296,7 +302,7 @@ class Problem:
 
     def assign(self, theta, *, with_margin: bool = False):
         """Tie-tolerant hard assignment (1-based labels) without the N x P costs."""
-        t, tflag = self._theta(theta)  # (pgx_assign always runs the exact fp64 kernels)
+        t, tflag = self._theta(theta)  # (tc problems: the sweep's ASSIGN variant; else the exact fp64 kernels)
         labels = np.empty(self.n_points, dtype=np.int64)
         margin = np.empty(self.n_points, dtype=np.float32) if with_margin else None
         with self._lock:

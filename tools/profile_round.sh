@@ -50,6 +50,7 @@ if len(rows) > 2:
     for r in rows[2:]:
         d, u = dict(zip(h, r)), dict(zip(h, units))
         kern = d["Kernel Name"].split("<")[0].replace("void ", "").replace("pgx::", "").replace("k_", "", 1)
+        kern = {"tc_sweep": "tc_pass1", "tc_grad": "tc_pass2"}.get(kern, kern)  # bench.py's kernel names
         res[f"{cfg}_{prec}:{kern}"] = {
             "dram_bytes_read": float(d["dram__bytes_read.sum"]) * scale[u["dram__bytes_read.sum"]],
             "dram_bytes_write": float(d["dram__bytes_write.sum"]) * scale[u["dram__bytes_write.sum"]],
