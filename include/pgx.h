@@ -192,6 +192,43 @@ size_t pgx_problem_bytes(pgx_problem* problem);
 enum { PGX_PATH_GENERAL = 0, PGX_PATH_GRID_FP64 = 1, PGX_PATH_GRID_TC = 2 };
 int pgx_problem_path(pgx_problem* problem);
 
+/* ---- Device-resident optimiser state.
+ * The fit loop of the reference (optimizer.py:195-342: L-BFGS two-loop
+ * recursion, strong-Wolfe line search, gauge fixing by the zero last column)
+ * keeps its decisions on the host; these calls keep its VECTORS on the GPU: the
+ * free parameters u = theta[:, :N-1], the gradient, the search direction and
+ * the (s, y) history.  Each call returns a handful of scalars.  A line-search
+ * trial (u + t d -> theta, pgx_eval, g_t . d) replays one captured CUDA graph.
+ * All reductions are fixed-order: identical inputs give identical trajectories.
+ *
+ * pgx_lbfgs_start   u <- theta[:, :N-1] (theta: K x N fp64, host), history cleared, evaluate:
+ *                   out[0..6] = {Phi, 0, err, e0, n_nonfinite, stats flags, |g|^2}
+ * pgx_lbfgs_restart re-evaluate the current point at a new eps (annealing); history cleared
+ * pgx_lbfgs_direction mode 0: d = two-loop(g) (optimizer.py:253-269; g/|g|^2 without history),
+ *                   1: d = g/|g|^2, 2: d = g; out[0..3] = {g.d, |d|^2, |g|^2, pairs used}
+ * pgx_lbfgs_trial   evaluate at u + t d: out[0..6] = {Phi, g_t.d, err, e0, n_nonfinite, flags, |g_t|^2}
+ * pgx_lbfgs_accept  the LAST trial point becomes current; with keep_pair the pair
+ *                   s = u_t - u, y = g - g_t joins the history when
+ *                   s.y > 1e-10 |s| |y| (optimizer.py:303-309);
+ *                   out[0..3] = {|g|^2, pushed (0/1), |u|^2, s.y}
+ * pgx_lbfgs_theta   the current point as a K x N fp64 host matrix (last column zero)
+ * pgx_lbfgs_iterate one iteration's device work in ONE submission and synchronisation:
+ *                   [accept the last trial when keep_pair >= 0] -> two-loop direction ->
+ *                   trial at u + t0 d; out[0..3] accept, out[4..7] direction, out[8..14]
+ *                   trial scalars (each laid out as in the single calls) */
+typedef struct pgx_lbfgs pgx_lbfgs;
+pgx_status pgx_lbfgs_create(pgx_problem* problem, int memory, pgx_lbfgs** out);
+void pgx_lbfgs_destroy(pgx_lbfgs* state);
+pgx_status pgx_lbfgs_start(pgx_lbfgs* state, const double* theta, double eps, double lambda, double* out);
+pgx_status pgx_lbfgs_restart(pgx_lbfgs* state, double eps, double lambda, double* out);
+pgx_status pgx_lbfgs_clear(pgx_lbfgs* state);
+pgx_status pgx_lbfgs_direction(pgx_lbfgs* state, int mode, double* out);
+pgx_status pgx_lbfgs_trial(pgx_lbfgs* state, double t, double eps, double lambda, double* out);
+pgx_status pgx_lbfgs_accept(pgx_lbfgs* state, int keep_pair, double* out);
+pgx_status pgx_lbfgs_theta(pgx_lbfgs* state, double* theta_out);
+pgx_status pgx_lbfgs_iterate(pgx_lbfgs* state, int keep_pair, double t0, double eps, double lambda,
+                             double* out);
+
 /* Number of kernel launches the last pgx_eval / pgx_assign enqueued. */
 int pgx_last_launch_count(pgx_problem* problem);
 

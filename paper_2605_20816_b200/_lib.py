@@ -94,6 +94,16 @@ SIGNATURES = {
     "pgx_set_stream": (c_int, [c_void_p, c_void_p]),
     "pgx_eval": (c_int, [c_void_p, c_void_p, c_double, c_double, c_uint32, c_void_p, c_void_p]),
     "pgx_assign": (c_int, [c_void_p, c_void_p, c_uint32, c_void_p, c_void_p, c_void_p]),
+    "pgx_lbfgs_create": (c_int, [c_void_p, c_int, ctypes.POINTER(c_void_p)]),
+    "pgx_lbfgs_destroy": (None, [c_void_p]),
+    "pgx_lbfgs_start": (c_int, [c_void_p, c_void_p, c_double, c_double, c_void_p]),
+    "pgx_lbfgs_restart": (c_int, [c_void_p, c_double, c_double, c_void_p]),
+    "pgx_lbfgs_clear": (c_int, [c_void_p]),
+    "pgx_lbfgs_direction": (c_int, [c_void_p, c_int, c_void_p]),
+    "pgx_lbfgs_trial": (c_int, [c_void_p, c_double, c_double, c_double, c_void_p]),
+    "pgx_lbfgs_accept": (c_int, [c_void_p, c_int, c_void_p]),
+    "pgx_lbfgs_theta": (c_int, [c_void_p, c_void_p]),
+    "pgx_lbfgs_iterate": (c_int, [c_void_p, c_int, c_double, c_double, c_double, c_void_p]),
     "pgx_last_launch_count": (c_int, [c_void_p]),
     "pgx_problem_path": (c_int, [c_void_p]),
     "pgx_set_profiling": (c_int, [c_void_p, c_int]),

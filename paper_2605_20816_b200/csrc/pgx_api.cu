@@ -782,4 +782,332 @@ pgx_status pgx_soft_assign(pgx_problem* pb, const void* theta, double eps, uint3
   return PGX_OK;
 }
 
+// ------------------------------------------------------------------ device-resident optimiser state
+// (kernels in k_lbfgs.cu)
+struct pgx_lbfgs {
+  pgx_problem* pb = nullptr;
+  int m = 10;
+  int64_t n = 0;  // K (N - 1) free parameters
+  double *u = nullptr, *g = nullptr, *ut = nullptr, *gt = nullptr, *d = nullptr;
+  double *S = nullptr, *Y = nullptr, *rho = nullptr, *alpha = nullptr;
+  double *theta = nullptr, *grad = nullptr;  // K x N, what pgx_eval reads / writes
+  int* state = nullptr;                      // {head, count}
+  double* host = nullptr;                    // pinned + mapped: [0] t, [2..5] kernel scalars, [8..] pgx_stats
+  double* host_dev = nullptr;                // its device alias
+  bool have_dir = false;                     // d holds a direction (trial points are u + t d)
+  cudaGraphExec_t graph = nullptr;           // point -> pgx_eval -> after, for (eps, lambda, have_dir)
+  double g_eps = 0.0, g_lambda = 0.0;
+  bool g_dir = false;
+  // the legacy default stream cannot be captured: a problem on it runs the
+  // optimiser calls on this stream instead (every call synchronises before returning)
+  cudaStream_t own_stream = nullptr;
+  // accept -> two-loop -> first trial as one graph (pgx_lbfgs_iterate), for (eps, lambda, keep_pair)
+  cudaGraphExec_t it_graph = nullptr;
+  double it_eps = 0.0, it_lambda = 0.0;
+  int it_keep = -1;
+  void drop_graph() {
+    if (graph) cudaGraphExecDestroy(graph);
+    if (it_graph) cudaGraphExecDestroy(it_graph);
+    graph = nullptr;
+    it_graph = nullptr;
+  }
+};
+
+namespace {
+
+constexpr int kLbScal = 2, kLbStats = 8;  // offsets (in doubles) inside pgx_lbfgs::host
+constexpr int kLbDir = 24, kLbAcc = 28;   // pgx_lbfgs_iterate: direction / accept scalars
+
+// runs the problem on the state's own stream while a call is in progress (see own_stream)
+struct LbStream {
+  pgx_problem* pb;
+  cudaStream_t saved;
+  explicit LbStream(pgx_lbfgs* st) : pb(st->pb), saved(st->pb->stream) {
+    if (!saved || saved == cudaStreamLegacy) {
+      cudaStreamSynchronize(saved);
+      pb->stream = st->own_stream;
+    }
+  }
+  ~LbStream() { pb->stream = saved; }
+};
+
+// enqueue: theta <- u (+ t d); evaluate; pack the free-column gradient and its dot products
+pgx_status lb_enqueue(pgx_lbfgs* st, double eps, double lambda) {
+  pgx_problem* pb = st->pb;
+  launch_lb_point(st->theta, st->ut, st->u, st->have_dir ? st->d : nullptr, st->host_dev, pb->K, pb->N,
+                  pb->sms, pb->stream);
+  PGX_LAUNCH_CHECK();
+  pgx_status rc = eval_impl(pb, st->theta, eps, lambda, PGX_WANT_GRAD | PGX_WANT_ASSIGN | PGX_DEVICE_PTRS,
+                            st->grad, reinterpret_cast<pgx_stats*>(st->host_dev + kLbStats), false);
+  if (rc != PGX_OK) return rc;
+  launch_lb_after(st->grad, st->gt, st->have_dir ? st->d : nullptr, st->host_dev + kLbScal, pb->K, pb->N,
+                  pb->stream);
+  PGX_LAUNCH_CHECK();
+  return PGX_OK;
+}
+
+// one evaluation at u + t d through the captured graph (re-captured when eps,
+// lambda or the kind of point changes); out = {phi, g_t.d, err, e0, n_nonfinite, flags, |g_t|^2}
+pgx_status lb_evaluate(pgx_lbfgs* st, double t, double eps, double lambda, double* out) {
+  pgx_problem* pb = st->pb;
+  PGX_CUDA(cudaSetDevice(pb->device));
+  static const bool use_graph = [] {
+    const char* e = std::getenv("PGX_FIT_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  st->host[0] = t;
+  if (use_graph && !pb->profiling) {
+    if (!st->graph || st->g_eps != eps || st->g_lambda != lambda || st->g_dir != st->have_dir) {
+      st->drop_graph();
+      // (the first evaluation of a problem runs its one-time set-up launches: not captured)
+      pgx_status rc = lb_enqueue(st, eps, lambda);
+      if (rc != PGX_OK) return rc;
+      PGX_CUDA(cudaStreamSynchronize(pb->stream));
+      cudaGraph_t gr = nullptr;
+      PGX_CUDA(cudaStreamBeginCapture(pb->stream, cudaStreamCaptureModeThreadLocal));
+      rc = lb_enqueue(st, eps, lambda);
+      cudaError_t ce = cudaStreamEndCapture(pb->stream, &gr);
+      if (rc != PGX_OK || ce != cudaSuccess) {
+        if (gr) cudaGraphDestroy(gr);
+        (void)cudaGetLastError();
+        return rc != PGX_OK ? rc : fail(PGX_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+      }
+      ce = cudaGraphInstantiate(&st->graph, gr, 0);
+      cudaGraphDestroy(gr);
+      if (ce != cudaSuccess) return fail(PGX_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(ce));
+      st->g_eps = eps;
+      st->g_lambda = lambda;
+      st->g_dir = st->have_dir;
+      // (the uncaptured run above already evaluated this point: its results stand)
+    } else {
+      PGX_CUDA(cudaGraphLaunch(st->graph, pb->stream));
+    }
+  } else {
+    pgx_status rc = lb_enqueue(st, eps, lambda);
+    if (rc != PGX_OK) return rc;
+  }
+  PGX_CUDA(cudaStreamSynchronize(pb->stream));
+  const pgx_stats* ps = reinterpret_cast<const pgx_stats*>(st->host + kLbStats);
+  out[0] = ps->phi;
+  out[1] = st->host[kLbScal];
+  out[2] = ps->err;
+  out[3] = ps->e0;
+  out[4] = (double)ps->n_nonfinite;
+  out[5] = (double)ps->flags;
+  out[6] = st->host[kLbScal + 1];
+  return PGX_OK;
+}
+
+}  // namespace
+
+void pgx_lbfgs_destroy(pgx_lbfgs* st) {
+  if (!st) return;
+  st->drop_graph();
+  void* bufs[] = {st->u, st->g, st->ut, st->gt, st->d, st->S, st->Y, st->rho, st->alpha, st->theta, st->grad,
+                  st->state};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (st->host) cudaFreeHost(st->host);
+  if (st->own_stream) cudaStreamDestroy(st->own_stream);
+  delete st;
+}
+
+pgx_status pgx_lbfgs_create(pgx_problem* pb, int memory, pgx_lbfgs** out) {
+  g_last_error.clear();
+  if (!pb || !out) return fail(PGX_ERR_INVALID_ARGUMENT, "problem and out must not be NULL");
+  if (memory < 1 || memory > 256) return fail(PGX_ERR_INVALID_ARGUMENT, "memory must lie in 1..256");
+  if (!pb->has_labels) return fail(PGX_ERR_INVALID_ARGUMENT, "problem was created without labels");
+  PGX_CUDA(cudaSetDevice(pb->device));
+  pgx_lbfgs* st = new pgx_lbfgs();
+  st->pb = pb;
+  st->m = memory;
+  st->n = (int64_t)pb->K * (pb->N - 1);
+  const size_t n = (size_t)st->n, kn = (size_t)pb->K * pb->N, ring = (size_t)memory + 1;
+  cudaError_t e = cudaSuccess;
+  auto alloc = [&](double** p, size_t cnt) {
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(1, cnt) * 8);
+    if (e == cudaSuccess) e = cudaMemset(*p, 0, std::max<size_t>(1, cnt) * 8);
+  };
+  alloc(&st->u, n), alloc(&st->g, n), alloc(&st->ut, n), alloc(&st->gt, n), alloc(&st->d, n);
+  alloc(&st->S, ring * n), alloc(&st->Y, ring * n), alloc(&st->rho, ring), alloc(&st->alpha, ring);
+  alloc(&st->theta, kn), alloc(&st->grad, kn);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&st->state), 2 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(st->state, 0, 2 * sizeof(int));
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st->own_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&st->host), 64 * 8, cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&st->host_dev), st->host, 0);
+  if (e != cudaSuccess) {
+    pgx_lbfgs_destroy(st);
+    return fail(e == cudaErrorMemoryAllocation ? PGX_ERR_RESOURCE : PGX_ERR_CUDA,
+                "optimiser state (%zu bytes): %s", (2 * ring + 5) * n * 8 + 2 * kn * 8, cudaGetErrorString(e));
+  }
+  std::memset(st->host, 0, 64 * 8);
+  *out = st;
+  return PGX_OK;
+}
+
+pgx_status pgx_lbfgs_start(pgx_lbfgs* st, const double* theta, double eps, double lambda, double* out) {
+  g_last_error.clear();
+  if (!st || !theta || !out) return fail(PGX_ERR_INVALID_ARGUMENT, "state, theta and out must not be NULL");
+  LbStream stream_scope(st);
+  pgx_problem* pb = st->pb;
+  PGX_CUDA(cudaSetDevice(pb->device));
+  // u <- the free columns of the host theta (K x N): staged through st->grad
+  PGX_CUDA(cudaMemcpyAsync(st->grad, theta, (size_t)pb->K * pb->N * 8, cudaMemcpyHostToDevice, pb->stream));
+  launch_lb_after(st->grad, st->u, nullptr, st->host_dev + kLbScal, pb->K, pb->N, pb->stream);
+  PGX_LAUNCH_CHECK();
+  PGX_CUDA(cudaMemsetAsync(st->state, 0, 2 * sizeof(int), pb->stream));
+  PGX_CUDA(cudaMemsetAsync(st->theta, 0, (size_t)pb->K * pb->N * 8, pb->stream));
+  st->have_dir = false;
+  return pgx_lbfgs_restart(st, eps, lambda, out);
+}
+
+pgx_status pgx_lbfgs_restart(pgx_lbfgs* st, double eps, double lambda, double* out) {
+  g_last_error.clear();
+  if (!st || !out) return fail(PGX_ERR_INVALID_ARGUMENT, "state and out must not be NULL");
+  LbStream stream_scope(st);
+  pgx_problem* pb = st->pb;
+  PGX_CUDA(cudaSetDevice(pb->device));
+  PGX_CUDA(cudaMemsetAsync(st->state, 0, 2 * sizeof(int), pb->stream));  // drop the history
+  st->have_dir = false;
+  pgx_status rc = lb_evaluate(st, 0.0, eps, lambda, out);
+  if (rc != PGX_OK) return rc;
+  // the evaluated point becomes the current one: g <- g_t (u_t == u)
+  PGX_CUDA(cudaMemcpyAsync(st->g, st->gt, (size_t)st->n * 8, cudaMemcpyDeviceToDevice, pb->stream));
+  PGX_CUDA(cudaStreamSynchronize(pb->stream));
+  return PGX_OK;
+}
+
+pgx_status pgx_lbfgs_clear(pgx_lbfgs* st) {
+  g_last_error.clear();
+  if (!st) return fail(PGX_ERR_INVALID_ARGUMENT, "state must not be NULL");
+  LbStream stream_scope(st);
+  PGX_CUDA(cudaSetDevice(st->pb->device));
+  PGX_CUDA(cudaMemsetAsync(st->state, 0, 2 * sizeof(int), st->pb->stream));
+  return PGX_OK;
+}
+
+pgx_status pgx_lbfgs_direction(pgx_lbfgs* st, int mode, double* out) {
+  g_last_error.clear();
+  if (!st || !out) return fail(PGX_ERR_INVALID_ARGUMENT, "state and out must not be NULL");
+  LbStream stream_scope(st);
+  if (mode < 0 || mode > 2) return fail(PGX_ERR_INVALID_ARGUMENT, "mode must be 0, 1 or 2");
+  pgx_problem* pb = st->pb;
+  PGX_CUDA(cudaSetDevice(pb->device));
+  launch_lb_two_loop(st->g, st->d, st->S, st->Y, st->rho, st->alpha, st->state, st->m, st->n, mode,
+                     st->host_dev + kLbScal, pb->stream);
+  PGX_LAUNCH_CHECK();
+  PGX_CUDA(cudaStreamSynchronize(pb->stream));
+  for (int i = 0; i < 4; ++i) out[i] = st->host[kLbScal + i];
+  st->have_dir = true;
+  return PGX_OK;
+}
+
+pgx_status pgx_lbfgs_trial(pgx_lbfgs* st, double t, double eps, double lambda, double* out) {
+  g_last_error.clear();
+  if (!st || !out) return fail(PGX_ERR_INVALID_ARGUMENT, "state and out must not be NULL");
+  LbStream stream_scope(st);
+  if (!st->have_dir) return fail(PGX_ERR_INVALID_ARGUMENT, "no search direction: call pgx_lbfgs_direction first");
+  return lb_evaluate(st, t, eps, lambda, out);
+}
+
+pgx_status pgx_lbfgs_accept(pgx_lbfgs* st, int keep_pair, double* out) {
+  g_last_error.clear();
+  if (!st || !out) return fail(PGX_ERR_INVALID_ARGUMENT, "state and out must not be NULL");
+  LbStream stream_scope(st);
+  pgx_problem* pb = st->pb;
+  PGX_CUDA(cudaSetDevice(pb->device));
+  launch_lb_accept(st->u, st->g, st->ut, st->gt, st->S, st->Y, st->rho, st->state, st->m, st->n, 1e-10,
+                   keep_pair, st->host_dev + kLbScal, pb->stream);
+  PGX_LAUNCH_CHECK();
+  PGX_CUDA(cudaStreamSynchronize(pb->stream));
+  for (int i = 0; i < 4; ++i) out[i] = st->host[kLbScal + i];
+  return PGX_OK;
+}
+
+// One L-BFGS iteration's device work in ONE submission and one synchronisation:
+// [accept the last trial (keep_pair >= 0)] -> two-loop direction -> trial at u + t0 d.
+// out[0..3] accept scalars (as pgx_lbfgs_accept; zeros without accept),
+// out[4..7] direction scalars (as pgx_lbfgs_direction), out[8..14] trial scalars
+// (as pgx_lbfgs_trial).  The host then runs its line search from the first trial.
+pgx_status pgx_lbfgs_iterate(pgx_lbfgs* st, int keep_pair, double t0, double eps, double lambda, double* out) {
+  g_last_error.clear();
+  if (!st || !out) return fail(PGX_ERR_INVALID_ARGUMENT, "state and out must not be NULL");
+  LbStream stream_scope(st);
+  pgx_problem* pb = st->pb;
+  PGX_CUDA(cudaSetDevice(pb->device));
+  static const bool use_graph = [] {
+    const char* e = std::getenv("PGX_FIT_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  st->host[0] = t0;
+  auto enqueue = [&]() -> pgx_status {
+    if (keep_pair >= 0) {
+      launch_lb_accept(st->u, st->g, st->ut, st->gt, st->S, st->Y, st->rho, st->state, st->m, st->n, 1e-10,
+                       keep_pair, st->host_dev + kLbAcc, pb->stream);
+      PGX_LAUNCH_CHECK();
+    }
+    launch_lb_two_loop(st->g, st->d, st->S, st->Y, st->rho, st->alpha, st->state, st->m, st->n, 0,
+                       st->host_dev + kLbDir, pb->stream);
+    PGX_LAUNCH_CHECK();
+    st->have_dir = true;
+    return lb_enqueue(st, eps, lambda);
+  };
+  if (use_graph && !pb->profiling && st->graph) {  // (the plain trial graph exists: set-up launches are done)
+    if (!st->it_graph || st->it_eps != eps || st->it_lambda != lambda || st->it_keep != keep_pair) {
+      if (st->it_graph) cudaGraphExecDestroy(st->it_graph);
+      st->it_graph = nullptr;
+      cudaGraph_t gr = nullptr;
+      PGX_CUDA(cudaStreamBeginCapture(pb->stream, cudaStreamCaptureModeThreadLocal));
+      pgx_status rc = enqueue();
+      cudaError_t ce = cudaStreamEndCapture(pb->stream, &gr);
+      if (rc != PGX_OK || ce != cudaSuccess) {
+        if (gr) cudaGraphDestroy(gr);
+        (void)cudaGetLastError();
+        return rc != PGX_OK ? rc : fail(PGX_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+      }
+      ce = cudaGraphInstantiate(&st->it_graph, gr, 0);
+      cudaGraphDestroy(gr);
+      if (ce != cudaSuccess) return fail(PGX_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(ce));
+      st->it_eps = eps;
+      st->it_lambda = lambda;
+      st->it_keep = keep_pair;
+    }
+    st->have_dir = true;
+    PGX_CUDA(cudaGraphLaunch(st->it_graph, pb->stream));
+  } else {
+    pgx_status rc = enqueue();
+    if (rc != PGX_OK) return rc;
+  }
+  PGX_CUDA(cudaStreamSynchronize(pb->stream));
+  const pgx_stats* ps = reinterpret_cast<const pgx_stats*>(st->host + kLbStats);
+  for (int i = 0; i < 4; ++i) out[i] = keep_pair >= 0 ? st->host[kLbAcc + i] : 0.0;
+  for (int i = 0; i < 4; ++i) out[4 + i] = st->host[kLbDir + i];
+  out[8] = ps->phi;
+  out[9] = st->host[kLbScal];
+  out[10] = ps->err;
+  out[11] = ps->e0;
+  out[12] = (double)ps->n_nonfinite;
+  out[13] = (double)ps->flags;
+  out[14] = st->host[kLbScal + 1];
+  return PGX_OK;
+}
+
+pgx_status pgx_lbfgs_theta(pgx_lbfgs* st, double* theta_out) {
+  g_last_error.clear();
+  if (!st || !theta_out) return fail(PGX_ERR_INVALID_ARGUMENT, "state and theta_out must not be NULL");
+  LbStream stream_scope(st);
+  pgx_problem* pb = st->pb;
+  PGX_CUDA(cudaSetDevice(pb->device));
+  // theta <- u (the current point, not the last trial)
+  const bool dir = st->have_dir;
+  st->have_dir = false;
+  launch_lb_point(st->theta, st->ut, st->u, nullptr, st->host_dev, pb->K, pb->N, pb->sms, pb->stream);
+  st->have_dir = dir;
+  PGX_LAUNCH_CHECK();
+  PGX_CUDA(cudaMemcpyAsync(theta_out, st->theta, (size_t)pb->K * pb->N * 8, cudaMemcpyDeviceToHost, pb->stream));
+  PGX_CUDA(cudaStreamSynchronize(pb->stream));
+  return PGX_OK;
+}
+
 }  // extern "C"

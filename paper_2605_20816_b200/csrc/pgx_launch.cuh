@@ -89,6 +89,18 @@ void launch_general_soft(const EvalParams& prm, double* prob, cudaStream_t s);
 cudaError_t launch_label_moments_i32(int M, int64_t P, const int32_t* labels0, int N,
                                      unsigned long long* out, int* bad, int sms, cudaStream_t s);
 
+// device-resident optimiser vectors (k_lbfgs.cu)
+void launch_lb_point(double* theta, double* ut, const double* u, const double* d, const double* t_ptr, int K,
+                     int N, int sms, cudaStream_t s);
+void launch_lb_after(const double* grad, double* gt, const double* d, double* out, int K, int N,
+                     cudaStream_t s);
+void launch_lb_two_loop(const double* g, double* d, const double* S, const double* Y, const double* rho,
+                        double* alpha, const int* state, int m, int64_t n, int mode, double* out,
+                        cudaStream_t s);
+void launch_lb_accept(double* u, double* g, const double* ut, const double* gt, double* S, double* Y,
+                      double* rho, int* state, int m, int64_t n, double skip, int keep_pair, double* out,
+                      cudaStream_t s);
+
 // regular-grid fp64 path: pgx_grid_pass1.cuh, pgx_grid_pass2.cuh
 template <int DIM, int D>
 void grid_dispatch_pass1(const GridParams& g, int R, int blocks, cudaStream_t s);

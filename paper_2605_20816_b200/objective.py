@@ -178,6 +178,9 @@ class Problem:
         return self._h
 
     def close(self):
+        for st in list(self.__dict__.get("_fit_states", {}).values()):  # cached optimiser states
+            st.close()
+        self.__dict__.pop("_fit_states", None)
         if getattr(self, "_exact", None) is not None:
             self._exact.close()
             self._exact = None

@@ -18,6 +18,16 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 
+
+
+@pytest.fixture(scope="module")
+def pgb():
+    import paper_2605_20816_b200 as m
+
+    m._lib.load()
+    return m
+
+
 WOLFE_C1 = 1e-4       # optimizer.py:29
 MAX_LINE_EVALS = 25   # optimizer.py:31
 
@@ -161,3 +171,98 @@ def test_workspace_bytes_match_allocation(cfg, prec):
     got = prob.device_bytes()
     prob.close()
     assert abs(est - got) <= 0.02 * got + 65536, (est, got)
+
+
+# ---------------------------------------------------------------- device-resident optimiser state
+def test_device_loop_two_loop_matches_numpy(pgb):
+    """pgx_lbfgs_direction (the fused two-loop kernel, optimizer.py:253-269)
+    against a NumPy two-loop on the same (s, y) history, through a real fit state."""
+    from paper_2605_20816_b200 import configs
+    from paper_2605_20816_b200.optimizer import _DeviceState
+
+    w = configs.c1(labeler="host")
+    prob = pgb.Problem(w.grid, w.kind, w.degree, w.n_grains, w.labels0, precision="exact")
+    dev = _DeviceState(prob, 4, 0.0)
+    rng = np.random.default_rng(0)
+    theta = np.zeros((w.K, w.n_grains))
+    theta[:, :-1] = 0.05 * rng.normal(size=(w.K, w.n_grains - 1))
+    n = w.n_grains
+    s_hist, y_hist = [], []
+
+    def grad_at(th):
+        res, _ = prob.eval(th, w.eps, want_grad=True, want_assign=True)
+        return res.phi, res.grad[:, : n - 1].ravel()
+
+    phi, err, e0, gg = dev.start(theta, w.eps)
+    p_ref, g = grad_at(theta)
+    assert phi == p_ref and gg == pytest.approx(float(g @ g), rel=1e-13)
+    u = theta[:, : n - 1].ravel().copy()
+    for it in range(7):  # more pairs than the memory: the ring wraps
+        slope0, dd, gg, used = dev.direction(0)
+        assert used == min(len(s_hist), 4)
+        if s_hist:
+            q = g.copy()
+            alphas = []
+            for s_v, y_v in zip(reversed(s_hist[-4:]), reversed(y_hist[-4:])):
+                a = (s_v @ q) / (s_v @ y_v)
+                q -= a * y_v
+                alphas.append(a)
+            r = (s_hist[-1] @ y_hist[-1]) / (y_hist[-1] @ y_hist[-1]) * q
+            for s_v, y_v, a in zip(s_hist[-4:], y_hist[-4:], reversed(alphas)):
+                r += s_v * (a - (y_v @ r) / (s_v @ y_v))
+            d = r
+        else:
+            d = g / (g @ g)
+        assert slope0 == pytest.approx(float(g @ d), rel=1e-9)
+        assert dd == pytest.approx(float(d @ d), rel=1e-9)
+        t = 0.5
+        p_t, s_t, e_t, z_t, gg_t, _ = dev.trial(t, w.eps)
+        th_t = np.zeros_like(theta)
+        th_t[:, : n - 1] = (u + t * d).reshape(w.K, n - 1)
+        p_ref, g_t = grad_at(th_t)
+        assert p_t == pytest.approx(p_ref, rel=1e-12)
+        assert s_t == pytest.approx(float(g_t @ d), rel=1e-8, abs=1e-14)
+        gg2, pushed, uu = dev.accept(True)
+        s_v, y_v = t * d, g - g_t
+        assert pushed == bool(s_v @ y_v > 1e-10 * np.linalg.norm(s_v) * np.linalg.norm(y_v))
+        if pushed:
+            s_hist.append(s_v)
+            y_hist.append(y_v)
+        u, g = u + t * d, g_t
+        assert np.allclose(dev.theta()[:, : n - 1].ravel(), u, rtol=1e-13, atol=1e-15)
+        assert np.all(dev.theta()[:, -1] == 0.0)
+    dev.close()
+    prob.close()
+
+
+def test_device_loop_range_fallback(pgb):
+    """A theta beyond the fast modes' logit range (theta x 1e8) moves the
+    device-resident fit onto the exact kernels instead of returning -inf."""
+    from paper_2605_20816_b200 import configs
+
+    w = configs.c1(labeler="host")
+    gm = pgb.GrainMap(grid=pgb.make_grid(64), labels=w.labels0 + 1, n_grains=20)
+    rng = np.random.default_rng(3)
+    vals = 1e8 * rng.normal(size=(3, 20))
+    vals[:, -1] = 0.0
+    init = pgb.ParamMatrix(vals, pgb.DesignBasis.make("legendre", 1), gauge=pgb.GAUGE_LAST_ZERO)
+    cfg = dict(degree=1, eps=0.05, max_iters=3, init=init)
+    host = pgb.fit(gm, pgb.FitConfig(**cfg, precision="exact"))
+    dev = pgb.fit(gm, pgb.FitConfig(**cfg, precision="tc", device_loop=True))
+    assert np.isfinite(dev.phi_traj[0]) and dev.phi_traj[0] == pytest.approx(host.phi_traj[0], rel=1e-12)
+
+
+def test_device_loop_ascent_and_schedule(pgb):
+    """method='ascent' and an eps schedule on the device state follow the host loop."""
+    from paper_2605_20816_b200 import configs
+
+    w = configs.c1(labeler="host")
+    gm = pgb.GrainMap(grid=pgb.make_grid(64), labels=w.labels0 + 1, n_grains=20)
+    for extra in (dict(method="ascent", lam=1e-4), dict(eps_schedule=(0.2, 0.8), lam=1e-4)):
+        cfg = dict(degree=1, eps=0.05, max_iters=12, precision="exact", **extra)
+        host = pgb.fit(gm, pgb.FitConfig(**cfg))
+        dev = pgb.fit(gm, pgb.FitConfig(**cfg, device_loop=True))
+        a, b = np.asarray(host.phi_traj), np.asarray(dev.phi_traj)
+        assert a.shape == b.shape and host.stop_reason == dev.stop_reason
+        assert np.abs(a - b).max() <= 1e-9 * (1 + np.abs(a).max())
+        assert host.evaluations == dev.evaluations

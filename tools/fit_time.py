@@ -4,7 +4,8 @@ import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2605_20816_b200 as pgb
 from paper_2605_20816_b200 import configs
-cfg, iters = sys.argv[1], int(sys.argv[2])
+cfg = sys.argv[1]
+iters = int(sys.argv[2]) if len(sys.argv) > 2 else 100
 prec = sys.argv[3] if len(sys.argv) > 3 else "tc"
 w = configs.make(cfg, labeler="host" if cfg in ("c1", "c2") else "gpu")
 gm = pgb.GrainMap(grid=w.grid, labels=w.labels0 + 1, n_grains=w.n_grains)
