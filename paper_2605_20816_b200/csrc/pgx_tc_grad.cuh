@@ -45,13 +45,6 @@ constexpr int kGdBuf = 8;
 constexpr int kGdA = 3;    // coefficient-image slots (lines in flight)
 constexpr int kGdMmaWarp = kTc2Epi / 32, kGdLoadWarp = kGdMmaWarp + 1;
 constexpr int kGdThreads = kTc2Epi + 64;  // + MMA warp + loader warp
-// epilogue work split: true = every item is shared by all 8 warps (warp =
-// lane quarter x pixel half), so two finished S stages always wait ahead of
-// the epilogue; false = two groups of 4 warps on alternate items
-#ifndef PGX_GD_HALVES
-#define PGX_GD_HALVES 0
-#endif
-constexpr bool kGdHalves = PGX_GD_HALVES != 0;
 #ifdef PGX_GD_TRACE
 // experiment builds only (tools/gd_trace.py): clock64 stamps of one CTA's first 256 items
 __device__ long long gd_trace[14][256];
@@ -164,7 +157,7 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
     }
     for (int b = 0; b < kTc2S; ++b) {
       mbar_init(&bar_s[b], 1);
-      mbar_init(&bar_p[b], kGdHalves ? 8 : 4);  // the warps that write the tile's r'
+      mbar_init(&bar_p[b], 4);  // the four warps of the tile's group
     }
     mbar_init(&bar_end, 1);
     fence_mbar_init();
@@ -333,8 +326,8 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
     float inv = 0.0f;
     int li_inv = -1;               // line whose chunk scale `inv` is
     Cur c{0, 0, t0}, cf{0, 0, t0};  // current item; item whose group may be flushed (group 0)
-    if (!kGdHalves && grp == 1) c.next(ntiles);
-    for (; c.n < nitems; c.next(ntiles)) {
+    if (grp == 1) c.next(ntiles);
+    for (; c.n < nitems; c.next(ntiles), c.next(ntiles)) {
       if (c.li != li_inv) {
         li_inv = c.li;
         const int sB = __ldg(&g.tc_meta[(l0 + c.li) * g.tc_nchunks + blockIdx.x].x);
@@ -342,11 +335,11 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
       }
       const int st = c.n % kTc2S, b = c.n % kGdBuf;
       const float* rec0 = reinterpret_cast<const float*>(smem + L::REC_OFF + b * L::REC);
-      if (q == 0 && lane == 0 && (!kGdHalves || grp == 0)) GD_STAMP(5, c.n);
+      if (q == 0 && lane == 0) GD_STAMP(5, c.n);
       mbar_spin(sbar_s + 8u * st, (unsigned)(c.n / kTc2S) & 1u);
       tc_fence_after();
-      if (q == 0 && lane == 0 && (!kGdHalves || grp == 0)) GD_STAMP(0, c.n);
-      if (lane == 0 && (!kGdHalves || grp == 0)) GD_STAMP(10 + q, c.n);
+      if (q == 0 && lane == 0) GD_STAMP(0, c.n);
+      if (lane == 0) GD_STAMP(10 + q, c.n);
       // UMMA 1 of this item follows UMMA 2 of item n - 3: the groups ending
       // there are final
       if (grp == 0)
@@ -355,7 +348,7 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
       mbar_spin(sbar_f + 8u * b, (unsigned)(c.n / kGdBuf) & 1u);  // records visible
       const unsigned long long ninv2 = f2pack(-inv, -inv);
 #pragma unroll 1
-      for (int h = kGdHalves ? grp : 0; h < (kGdHalves ? grp + 1 : 2); ++h) {  // pixel halves [32 h, 32 h + 32)
+      for (int h = 0; h < 2; ++h) {  // pixel halves [32 h, 32 h + 32)
         const unsigned ts = tmem + 64u * st + lane_off + 32u * h;
         const float* rec = rec0 + 32 * h;
         uint32_t sv[32];
@@ -438,10 +431,9 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (q == 0 && lane == 0 && (!kGdHalves || grp == 0)) GD_STAMP(1, c.n);
-      if (lane == 0 && (!kGdHalves || grp == 0)) GD_STAMP(6 + q, c.n);
+      if (q == 0 && lane == 0) GD_STAMP(1, c.n);
+      if (lane == 0) GD_STAMP(6 + q, c.n);
       if (lane == 0) mbar_arrive(&bar_p[st]);
-      if (!kGdHalves) c.next(ntiles);
     }
     // the last groups: complete once the final commit lands
     if (grp == 0) {

@@ -25,7 +25,7 @@ from . import _lib
 from .basis import GAUGE_LAST_ZERO, LEGENDRE, MONOMIAL
 
 CHUNK_SIZE = 8192  # accepted for signature parity (objective.py:30); unused on the GPU
-DEFAULT_PRECISION = os.environ.get("PGX_PRECISION", "fp64")
+DEFAULT_PRECISION = os.environ.get("PGX_PRECISION", "tc")
 
 
 class EvalResult(NamedTuple):
