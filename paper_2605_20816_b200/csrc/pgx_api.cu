@@ -272,13 +272,21 @@ pgx_status validate_desc(const pgx_desc* d) {
   return PGX_OK;
 }
 
+// pass-2 point splits of the general kernels: up to 4 CTAs per SM and grain
+// tile, at least 128 points each (few grains leave most of a CTA's threads
+// idle: many short CTAs fill the SMs instead; the tail reduces the splits in
+// fixed order)
+int general_splits(int64_t P, int tiles, int sms) {
+  return std::max(1, std::min<int>(4 * sms / tiles, (int)std::min<int64_t>((P + 127) / 128, 1 << 20)));
+}
+
 size_t workspace_estimate(const pgx_desc* d, int sms) {
   const int64_t P = d->n_points;
   const int K = d->design ? d->design_k : feature_count(d->dim, d->degree);
   const int64_t KN = (int64_t)K * d->n_grains;
   const int64_t blocks1 = (P + kP1Threads - 1) / kP1Threads;
   const int tiles = (d->n_grains + kP2Threads - 1) / kP2Threads;
-  const int splits = std::max(1, std::min<int>(4 * sms / tiles, (int)((P + 1023) / 1024)));
+  const int splits = general_splits(P, tiles, sms);
   size_t b = 0;
   b += (d->resolution > 0 ? 0 : (size_t)P * d->dim * 8);
   b += (size_t)P * 4 + (size_t)KN * 8 * 3 + (size_t)P * 8 * 2 + (size_t)P * 4;
@@ -343,7 +351,7 @@ pgx_status pgx_problem_create(const pgx_desc* desc, pgx_problem** out) {
   const int64_t KN = (int64_t)pb->K * pb->N;
   pb->blocks1 = (int)((P + kP1Threads - 1) / kP1Threads);
   const int tiles = (pb->N + kP2Threads - 1) / kP2Threads;
-  pb->splits = std::max(1, std::min<int>(4 * sms / tiles, (int)((P + 1023) / 1024)));
+  pb->splits = general_splits(P, tiles, sms);
 
   cudaError_t e = cudaSuccess;
   auto A = [&](cudaError_t r) {

@@ -438,9 +438,33 @@ __global__ void __launch_bounds__(kSwThreads, 1) k_tc_sweep(GridParams g) {
         }
       // a third block as close (or an overflowing candidate list, or logits
       // beyond the fp32 range): exact re-scan in the tail
-      const bool found = st.cnt > 0 && !(st.flags & 2) && !(m3b <= m1 + wnd) && bmax <= 3e38f;
-      const double m2x = st.m2;  // exact runner-up among the candidates (+inf: a single candidate)
+      bool found = st.cnt > 0 && !(st.flags & 2) && !(m3b <= m1 + wnd) && bmax <= 3e38f;
+      double m2x = st.m2;  // exact runner-up among the candidates (+inf: a single candidate)
       st.m2 = fmin(st.m2, (double)(two ? m3b : m2b) - (double)delta);  // out-of-block runner-up bound
+      if (!found && bmax <= 3e38f) {
+        // more than two blocks (or more than two columns) within the window -- e.g. every
+        // pixel at theta = 0, the default start of a fit: decide here with an exact fp64
+        // scan of the line's coefficient table (J FMAs per grain; all lanes of a warp read
+        // the same rows) instead of queueing the pixel for the tail's K-term re-scan
+        double em = CUDART_INF, em2 = CUDART_INF;
+        for (int i = 0; i < N; ++i) {
+          const double h = eval_line<J>(coef_line + (int64_t)i * J, u);
+          em2 = fmin(em2, fmax(em, h));
+          em = fmin(em, h);
+        }
+        const double thr = em + c * kTieRtol * (1.0 + fabs(em / c));
+        int best = 0;
+        for (int i = 0; i < N; ++i)
+          if (eval_line<J>(coef_line + (int64_t)i * J, u) <= thr) {
+            best = i;
+            break;
+          }
+        st.m = em;
+        st.m2 = m2x = em2;
+        st.b0 = best;
+        st.cnt = 1;
+        found = true;
+      }
       if constexpr (ASSIGN) {
         // (without candidates the tail's re-scan only needs an upper bound of the min)
         const double m = st.cnt > 0 ? st.m : (double)m1 + (double)delta;
