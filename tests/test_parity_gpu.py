@@ -40,6 +40,20 @@ def _grid_or_points(pgb, z):
     return pgb.make_grid(int(z["grid_m"]))
 
 
+def _expected_path(grid, prec, degree=1, dim=2):
+    """Which kernel family a (grid, precision) pair runs (pgx_problem_path): the
+    tcgen05 kernels on regular grids with side >= 64, the separable fp64 kernels on
+    sides that are a multiple of 128, the exact general kernels everywhere else --
+    a "tc" / "fp64" case on a point list or a tiny grid is a test of that fallback."""
+    res = getattr(grid, "resolution", None)
+    ok_deg = degree <= (8 if dim == 2 else 4)
+    if prec == "tc" and res is not None and 2 * res >= 64 and ok_deg:
+        return "grid_tc"
+    if prec == "fp64" and res is not None and (2 * res) % 128 == 0 and ok_deg:
+        return "grid_fp64"
+    return "general"
+
+
 def _assert_grad(z, j, grad, tol):
     if f"grad{j}" in z:
         ref = z[f"grad{j}"]
@@ -65,9 +79,13 @@ def test_golden_eval_and_assign(pgb, name, prec):
     labels0 = np.asarray(z["labels0"], dtype=np.int64)
     grid = _grid_or_points(pgb, z)
     prob = pgb.Problem(grid, kind, degree, n, labels0, precision=prec)
+    path = _expected_path(grid, prec, degree)
+    assert prob.kernel_path == path
     tphi, tgrad = TOL[prec]
     for j, th in enumerate(gl.thetas(z)):
-        res, st = prob.eval(th, eps, want_grad=True, want_assign=True)
+        res, st, names = prob.eval_kernels(th, eps, want_grad=True, want_assign=True)
+        want = {"grid_tc": "tc_pass1", "grid_fp64": "grid_pass1", "general": "general_pass1"}[path]
+        assert want in names, (path, names)
         phi_ref = float(z[f"phi{j}"])
         assert abs(res.phi - phi_ref) <= tphi * (1 + abs(phi_ref)), (j, res.phi, phi_ref)
         _assert_grad(z, j, res.grad, tgrad)
@@ -84,7 +102,8 @@ def test_golden_eval_and_assign(pgb, name, prec):
 
 @pytest.mark.parametrize("prec", PRECISIONS)
 def test_random_shapes_vs_oracle(pgb, prec):
-    """Ragged N/P, tiny cases, both bases, 2-D and 3-D, unstructured lists."""
+    """Ragged N/P, tiny cases, both bases, 2-D and 3-D, unstructured lists: every
+    precision request on a point list runs the exact general kernels (asserted)."""
     rng = np.random.default_rng(77)
     tphi, tgrad = TOL[prec]
     cases = [(2, 1, 2, 1, "legendre"), (2, 3, 3, 1, "monomial"), (2, 2, 7, 37, "legendre"),
@@ -99,6 +118,7 @@ def test_random_shapes_vs_oracle(pgb, prec):
         ref = oracle.evaluate_objective(th, oracle.design_values(kind, d, pts), labels0, eps,
                                         want_grad=True, want_assign=True)
         prob = pgb.Problem(pgb.PixelGrid(points=pts), kind, d, n, labels0, precision=prec)
+        assert prob.kernel_path == "general"
         res, st = prob.eval(th, eps, want_grad=True, want_assign=True)
         assert abs(res.phi - ref.phi) <= tphi * (1 + abs(ref.phi)), (dim, d, n, p)
         assert np.abs(res.grad - ref.grad).max() <= tgrad * max(np.abs(ref.grad).max(), 1e-300)
