@@ -163,3 +163,48 @@ def test_tc_padded_grid_vs_oracle(dim, m, d, n, eps):
         res2, _ = prob.eval(th, eps, want_grad=True, want_assign=True)
         assert res2.phi == res.phi and np.array_equal(res2.grad, res.grad)
     prob.close()
+
+
+# ---------------------------------------------------------------- randomized shapes on the tc path
+def test_tc_random_grid_shapes_vs_exact_kernels():
+    """Random sides (padded and not), grain counts (N % 32/64/128 != 0), degrees and
+    both bases on the tcgen05 path, against the oracle-pinned exact fp64 kernels:
+    evaluation, hard assignment, tie handling (duplicated and all-zero columns)."""
+    import paper_2605_20816_b200 as pgb
+
+    rng = np.random.default_rng(2026)
+    tphi, tgrad = TOL["tc"]
+    shapes = [(2, int(rng.integers(32, 160)), int(rng.integers(0, 9)), int(rng.integers(2, 700)))
+              for _ in range(10)]
+    shapes += [(3, int(rng.integers(32, 48)), int(rng.integers(0, 5)), int(rng.integers(2, 300)))
+               for _ in range(3)]
+    shapes += [(2, 64, 2, 2), (2, 32, 1, 513), (2, 97, 8, 129)]
+    for dim, m, d, n in shapes:
+        kind = "legendre" if rng.random() < 0.7 else "monomial"
+        k = oracle.feature_count(d, dim)
+        grid = pgb.make_grid(m, dim)
+        # labels with spatial structure (a random diagram + 1% noise), as in every real
+        # workload: with uniformly random labels the gradient at theta = 0 is pure sampling
+        # noise and the max-norm relative tolerance would only measure the MUFU bias
+        labels0 = _labels_from_diagram(rng, "legendre", max(d, 1), dim, m, n)
+        eps = float(10 ** rng.uniform(-2.3, -0.5))
+        tc = pgb.Problem(grid, kind, d, n, labels0, precision="tc")
+        ex = pgb.Problem(grid, kind, d, n, labels0, precision="exact")
+        assert tc.kernel_path == "grid_tc" and ex.kernel_path == "general"
+        thetas = [rng.normal(size=(k, n)) * 10 ** rng.uniform(-2, 0.5), np.zeros((k, n))]
+        dup = rng.normal(size=(k, n))
+        dup[:, n // 2] = dup[:, 0]  # an exact tie between two grains
+        thetas.append(dup)
+        for th in thetas:
+            a, sa = tc.eval(th, eps, lam=1e-4, want_grad=True, want_assign=True)
+            b, sb = ex.eval(th, eps, lam=1e-4, want_grad=True, want_assign=True)
+            tag = (dim, m, d, n, kind, eps)
+            assert abs(a.phi - b.phi) <= tphi * (1 + abs(b.phi)), tag
+            assert np.abs(a.grad - b.grad).max() <= tgrad * max(np.abs(b.grad).max(), 1e-300), tag
+            assert abs(a.err - b.err) * len(grid) <= max(sa.n_ambiguous, sb.n_ambiguous), tag
+            assert a.e0 == pytest.approx(b.e0, rel=1e-9, abs=1e-12), tag
+            la, lb = tc.assign(th), ex.assign(th)
+            bad = np.flatnonzero(la != lb)
+            assert len(bad) <= max(sa.n_ambiguous, sb.n_ambiguous), (tag, len(bad))
+        tc.close()
+        ex.close()
