@@ -1,5 +1,5 @@
 #!/bin/bash
-# round-2 state: GPU tests, smoke, default bench (c5 tc) + reference arm, c5 profile, quick lines
+# round state check (bash tools/gpu_round.sh TAG): GPU tests, smoke, default bench (c5 tc) + reference arm, c5 profile, quick lines
 mkdir -p gpurun_out
 TAG=${1:-r02f}
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest.txt 2>&1
