@@ -46,10 +46,14 @@ constexpr int kGdA = 3;    // coefficient-image slots (lines in flight)
 constexpr int kGdMmaWarp = kTc2Epi / 32, kGdLoadWarp = kGdMmaWarp + 1;
 constexpr int kGdThreads = kTc2Epi + 64;  // + MMA warp + loader warp
 #ifdef PGX_GD_TRACE
+#ifndef PGX_GD_TRACE_X  // the traced CTA
+#define PGX_GD_TRACE_X 3
+#define PGX_GD_TRACE_Y 5
+#endif
 // experiment builds only (tools/gd_trace.py): clock64 stamps of one CTA's first 256 items
 __device__ long long gd_trace[14][256];
 #define GD_STAMP(e, n) \
-  do { if (blockIdx.x == 3 && blockIdx.y == 5 && (n) < 256) gd_trace[e][n] = clock64(); } while (0)
+  do { if (blockIdx.x == PGX_GD_TRACE_X && blockIdx.y == PGX_GD_TRACE_Y && (n) < 256) gd_trace[e][n] = clock64(); } while (0)
 #else
 #define GD_STAMP(e, n) do { } while (0)
 #endif
