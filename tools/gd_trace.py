@@ -9,7 +9,10 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "c5"
 w = configs.make(cfg, labeler="host" if cfg in ("c1", "c2") else "gpu")
 prob = pgb.Problem(w.grid, w.kind, w.degree, w.n_grains, w.labels0, precision="tc")
 for _ in range(3):
-    prob.eval(w.theta_bench, w.eps, lam=w.lam, want_grad=True, want_assign=True)
+    try:
+        prob.eval(w.theta_bench, w.eps, lam=w.lam, want_grad=True, want_assign=True)
+    except Exception as exc:  # what-if builds produce garbage: only the stamps matter
+        print("eval:", type(exc).__name__)
 lib = _lib.load()
 buf = np.zeros((14, 256), dtype=np.int64)
 lib.pgx_debug_trace.argtypes = [ctypes.c_void_p]
