@@ -326,7 +326,7 @@ class _OracleProblem:
         return EvalResult(r.phi, r.grad, r.err, r.e0), None
 
 
-def fit_c1(problem, precision=None, device_loop=False, repeats=1):
+def fit_c1(problem, precision=None, device_loop=False, repeats=1, method="lbfgs"):
     """The reference fit at c1: 100 L-BFGS iterations
     (the last of `repeats` runs on one problem is reported: a fit's first run on a
     fresh GPU problem pays the one-time set-up launches and graph captures)."""
@@ -335,8 +335,11 @@ def fit_c1(problem, precision=None, device_loop=False, repeats=1):
 
     w = configs.c1(labeler="host")
     gm = pgb.GrainMap(grid=w.grid, labels=w.labels0 + 1, n_grains=w.n_grains)
+    # (BASELINE c1: eps = 0.05, lambda = 1e-4 with the ascent variant; the reference's own fit
+    # is L-BFGS at lambda = 0)
     cfg = pgb.FitConfig(degree=w.degree, basis_kind=w.kind, eps=w.eps, max_iters=100,
-                        precision=precision or "tc", device_loop=device_loop)
+                        precision=precision or "tc", device_loop=device_loop, method=method,
+                        lam=w.lam if method == "ascent" else 0.0)
     prob = problem(w) if callable(problem) else problem
     if prob is None and repeats > 1:
         prob = pgb.Problem(w.grid, w.kind, w.degree, w.n_grains, w.labels0, precision=precision or "tc")
@@ -346,7 +349,8 @@ def fit_c1(problem, precision=None, device_loop=False, repeats=1):
         dt = time.perf_counter() - t0
     return {"seconds": dt, "iterations": rep.iterations_run, "evaluations": rep.evaluations,
             "evals_per_s": rep.evaluations / dt, "phi_final": rep.phi_final, "stop": rep.stop_reason,
-            "loop": "device-resident state + CUDA graphs" if device_loop else "host", "runs": repeats}
+            "loop": "device-resident state + CUDA graphs" if device_loop else "host", "runs": repeats,
+            "method": method}
 
 
 def cpu_baseline_leg(w, seconds):
@@ -538,6 +542,8 @@ def run_ours(args):
         try:
             fit = fit_c1(None, args.precision, repeats=2)
             fit["device_loop"] = fit_c1(None, args.precision, device_loop=True, repeats=2)
+            fit["ascent_device_loop"] = fit_c1(None, args.precision, device_loop=True, repeats=2,
+                                               method="ascent")
         except Exception as exc:  # noqa: BLE001
             fit = {"error": repr(exc)}
 
