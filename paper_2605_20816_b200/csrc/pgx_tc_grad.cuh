@@ -87,6 +87,9 @@ __device__ __forceinline__ uint32_t pack_h2_ordered(float a, float b) {
   asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
   return r;
 }
+#ifndef PGX_GD_FLUSH32
+#define PGX_GD_FLUSH32 1  // the L_hi / L_lo halves of an fp32 group sum are added in fp32 (2^-24 relative)
+#endif
 #ifndef PGX_GD_ILV
 #define PGX_GD_ILV 1
 #endif
@@ -317,7 +320,8 @@ __global__ void __launch_bounds__(kGdThreads, 2) k_tc_grad(GridParams g) {
       tmem_regs_ready(rw);
 #pragma unroll
       for (int j = 0; j < J; ++j)
-        R64[j * kTc2Grains] += (double)__uint_as_float(rv[j]) + (double)__uint_as_float(rw[j]);
+        R64[j * kTc2Grains] += PGX_GD_FLUSH32 ? (double)(__uint_as_float(rv[j]) + __uint_as_float(rw[j]))
+                                              : (double)__uint_as_float(rv[j]) + (double)__uint_as_float(rw[j]);
       if (c.t == ntiles - 1 || c.n == nitems - 1) {  // the line's (or the CTA's) last item
         if (i < g.N) tc_grad_line<DIM, D>(acc, g.N, g.tc_lc + (l0 + c.li) * K, R64, c.li == 0);
 #pragma unroll
