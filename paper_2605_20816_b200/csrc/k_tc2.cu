@@ -8,10 +8,18 @@ namespace pgx {
 
 template <int DIM, int D>
 void tc_dispatch_coeffs(const GridParams& g, const GridPlan& gp, cudaStream_t s) {
-  dim3 grid(gp.lines, gp.tc_nchunks);
-  k_tc_coeffs<DIM, D><<<grid, kTcCoefChunk, 0, s>>>(g, gp.tc_coef, gp.tc_img,
-                                                    reinterpret_cast<TcCoefMeta*>(gp.tc_meta),
-                                                    gp.tc_nchunks);
+  constexpr int LPC = tc_coef_lines(DIM, D);
+  if constexpr (LPC > 1) {
+    dim3 grid((gp.lines + LPC - 1) / LPC, gp.tc_nchunks);
+    k_tc_coeffs_ml<DIM, D><<<grid, kTcCoefChunk, 0, s>>>(g, gp.tc_coef, gp.tc_img,
+                                                         reinterpret_cast<TcCoefMeta*>(gp.tc_meta),
+                                                         gp.tc_nchunks);
+  } else {
+    dim3 grid(gp.lines, gp.tc_nchunks);
+    k_tc_coeffs<DIM, D><<<grid, kTcCoefChunk, 0, s>>>(g, gp.tc_coef, gp.tc_img,
+                                                      reinterpret_cast<TcCoefMeta*>(gp.tc_meta),
+                                                      gp.tc_nchunks);
+  }
 }
 
 template <int DIM, int D>

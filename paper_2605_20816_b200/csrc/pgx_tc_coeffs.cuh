@@ -117,6 +117,119 @@ __global__ void __launch_bounds__(kTcCoefChunk) k_tc_coeffs(GridParams g, double
   }
 }
 
+// The same tables with several lines per CTA, for many features (K > 16): the chunk's
+// theta (K x 128) is read once into registers and serves kTcCoefLines lines.  Every
+// (line, chunk) CTA re-reading it made k_tc_coeffs L2-read bound at c5 (3 GB of theta
+// reads for 1.1 GB of table writes: 0.43 -> 0.35 ms); with few features the one-line
+// kernel above is faster (c4: 0.58 vs 0.68 ms), so the launcher picks (tc_coef_lines).
+constexpr int kTcCoefLines = 8;
+__host__ __device__ constexpr int tc_coef_lines(int dim, int degree) {
+  return feature_count(dim, degree) > 16 ? kTcCoefLines : 1;
+}
+
+template <int DIM, int D>
+__global__ void __launch_bounds__(kTcCoefChunk) k_tc_coeffs_ml(GridParams g, double* __restrict__ coef,
+                                                            unsigned char* __restrict__ img,
+                                                            TcCoefMeta* __restrict__ meta,
+                                                            int nchunks) {
+  constexpr int J = D + 1;
+  constexpr int K = feature_count(DIM, D);
+  constexpr int KS = tc_ksteps(J);
+  __shared__ double lc[tc_coef_lines(DIM, D)][K];
+  __shared__ unsigned s_max[tc_coef_lines(DIM, D)], s_b1[tc_coef_lines(DIM, D)];
+  const int tid = threadIdx.x;
+  // line groups on gridDim.x (3-D grids have side^2 > 65535 lines), chunks on y
+  const int chunk = blockIdx.y;
+  constexpr int LPC = tc_coef_lines(DIM, D);
+  const int64_t line0 = (int64_t)blockIdx.x * LPC;
+  const int nl = (int)min((int64_t)LPC, (int64_t)g.lines - line0);
+  const int i = chunk * kTcCoefChunk + tid;
+  if (tid < nl) {
+    double lcr[K];
+    line_factors<DIM, D>(line0 + tid, g, lcr);
+#pragma unroll
+    for (int k = 0; k < K; ++k) lc[tid][k] = lcr[k];
+    if (chunk == 0 && g.tc_lc) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) g.tc_lc[(line0 + tid) * K + k] = lcr[k];
+    }
+    s_max[tid] = 0u;
+    s_b1[tid] = 0u;
+  }
+  // this thread's grain: theta column i, widened exactly when fp32
+  double th[K];
+  if (i < g.N) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      th[k] = g.theta32 ? (double)__ldg(g.theta32 + (int64_t)k * g.N + i) : __ldg(g.theta + (int64_t)k * g.N + i);
+    if (g.theta32 && line0 == 0) {  // the fp64 theta every later kernel reads
+      double* th64 = const_cast<double*>(g.theta);
+#pragma unroll
+      for (int k = 0; k < K; ++k) th64[(int64_t)k * g.N + i] = th[k];
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k) th[k] = 0.0;
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int l = 0; l < nl; ++l) {
+    // B''_{j,i} = c * sum_{k: alpha_fast(k) = j} theta_{k,i} lc[k]: the order of line_coeffs
+    double B[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) B[j] = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int j = alpha_of(DIM, D, k, DIM - 1);
+      B[j] = fma(th[k], lc[l][k], B[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) B[j] *= g.c;
+    if (i < g.N) {
+      double* out = coef + ((line0 + l) * g.N + i) * J;
+#pragma unroll
+      for (int j = 0; j < J; ++j) out[j] = B[j];
+    }
+    float bm = 0.0f, b1 = 0.0f;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      bm = fmaxf(bm, (float)fabs(B[j]));
+      b1 += (float)fabs(B[j]);
+    }
+    // non-finite coefficients poison the scale; the passes then flag the pixels
+    atomicMax(&s_max[l], __float_as_uint(isfinite(bm) ? bm : CUDART_INF_F));
+    atomicMax(&s_b1[l], __float_as_uint(isfinite(b1) ? b1 * 1.0000005f : CUDART_INF_F));
+    __syncthreads();
+    const float chmax = __uint_as_float(s_max[l]);
+    const int sB = chmax > 0.0f && chmax < 3e38f ? 13 - ilogbf(chmax) : 0;
+    const double scl = ldexp(1.0, sB);
+    __half hi[J], lo[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) split_f16(B[j] * scl, hi[j], lo[j]);
+    unsigned char* dst = img + ((line0 + l) * nchunks + chunk) * (int64_t)tc_img_bytes<J>();
+    // row tid: 16 K-elements per slab = two 16-byte core-matrix rows
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      __half row[16];
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        const int k = s * 16 + kk;
+        const int b = k / J, j = k % J;
+        row[kk] = k < 3 * J ? (b == 1 ? lo[j] : hi[j]) : __float2half(0.0f);
+      }
+      unsigned char* slab = dst + s * (kTcCoefChunk * 32);
+      *reinterpret_cast<uint4*>(slab + slab_off(tid, 0)) = *reinterpret_cast<const uint4*>(row);
+      *reinterpret_cast<uint4*>(slab + slab_off(tid, 8)) = *reinterpret_cast<const uint4*>(row + 8);
+    }
+    if (tid == 0) {
+      TcCoefMeta m;
+      m.sB = sB;
+      m.bnorm = __uint_as_float(s_b1[l]);
+      meta[(line0 + l) * nchunks + chunk] = m;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ pixel tables
 // Pass-2 pixel operands of one 64-pixel tile of the fast axis (they depend on
 // the column only, so one table serves every line; built once per problem):
